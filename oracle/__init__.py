@@ -1,0 +1,141 @@
+"""fp64 CPU oracle for Sparse Feature Attention -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product path
+(``paper_2603_22300_b200``) never imports it, and the two share no code.
+
+``build()`` compiles ``sfa_oracle.c`` with gcc into ``liboracle.so`` next to it;
+the wrappers below only marshal numpy arrays (see sfa_oracle.c for the definitions
+and the PAPER.md passages each function follows).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sfa_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+F32, BF16 = 0, 1
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (plain C, -O2, no fast-math) into oracle/liboracle.so."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fno-fast-math", "-ffp-contract=off",
+             "-o", tmp, _SRC, "-lm", "-lpthread"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        P, I, L, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+        _lib.ref_topk_codes.argtypes = [P, I, L, I, I, P, P]
+        _lib.ref_topk_codes.restype = I
+        _lib.ref_attn_fwd.argtypes = [I, I, I, I, I, I, L, L, L, I, D, I, P, P, P, P, P, P, L, P, P, I]
+        _lib.ref_attn_fwd.restype = I
+        _lib.ref_scores_row.argtypes = [I, I, I, I, I, L, L, L, I, D, I, P, P, P, P, L, P]
+        _lib.ref_scores_row.restype = I
+        _lib.ref_edge_count.argtypes = [I, I, I, I, L, L, L, I, P, P]
+        _lib.ref_edge_count.restype = L
+    return _lib
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int):
+        super().__init__({1: "invalid-argument", 2: "invalid-input"}.get(code, f"status {code}"))
+        self.code = code
+
+
+def _ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p) if a is not None else None
+
+
+def _dtype_code(vals: np.ndarray) -> int:
+    if vals.dtype == np.float32:
+        return F32
+    if vals.dtype == np.uint16:  # bf16 bit patterns
+        return BF16
+    raise TypeError(f"oracle takes float32 or uint16 (bf16 bits), got {vals.dtype}")
+
+
+def topk_codes(x: np.ndarray, k: int):
+    """x: [rows, d] float32 or uint16 (bf16 bits).  Returns (idx u8 [rows,k], val [rows,k])."""
+    x = np.ascontiguousarray(x)
+    rows, d = x.shape
+    idx = np.zeros((rows, k), np.uint8)
+    val = np.zeros((rows, k), x.dtype)
+    st = _load().ref_topk_codes(_ptr(x), _dtype_code(x), rows, d, k, _ptr(idx), _ptr(val))
+    if st:
+        raise OracleError(st)
+    return idx, val
+
+
+def attn_fwd(q_idx, q_val, k_idx, k_val, v, *, d, causal=True, scale=None, q_pos0=0, rows=None,
+             threads=None):
+    """Plain fp64 SFA attention forward on the decompressed codes (sfa_oracle.c ref_attn_fwd).
+
+    q_idx/q_val [B,H,n_q,k]; k_idx/k_val [B,H_kv,n_kv,k]; v [B,H_kv,n_kv,d_v] (vals and v share a
+    dtype: float32 or uint16 bf16 bits).  ``d`` is the full head dimension.  ``rows``: optional
+    int64 flat row ids into [B,H,n_q].  Returns fp64 (o, lse), shaped [B,H,n_q,(d_v)] or [nsel,(d_v)].
+    """
+    q_idx = np.ascontiguousarray(q_idx); q_val = np.ascontiguousarray(q_val)
+    k_idx = np.ascontiguousarray(k_idx); k_val = np.ascontiguousarray(k_val)
+    v = np.ascontiguousarray(v)
+    B, H, n_q, k = q_idx.shape
+    _, H_kv, n_kv, _ = k_idx.shape
+    d_v = v.shape[-1]
+    dt = _dtype_code(q_val)
+    assert _dtype_code(k_val) == dt and _dtype_code(v) == dt
+    if scale is None:
+        scale = 1.0 / np.sqrt(d)  # A5: 1/sqrt(d), d the full head dimension
+    if rows is None:
+        sel, nsel = None, B * H * n_q
+        o = np.zeros((B, H, n_q, d_v), np.float64)
+        lse = np.zeros((B, H, n_q), np.float64)
+    else:
+        sel = np.ascontiguousarray(rows, dtype=np.int64)
+        nsel = sel.size
+        o = np.zeros((nsel, d_v), np.float64)
+        lse = np.zeros((nsel,), np.float64)
+    threads = threads or os.cpu_count() or 1
+    st = _load().ref_attn_fwd(B, H, H_kv, d, k, d_v, n_q, n_kv, q_pos0, int(bool(causal)), float(scale), dt,
+                              _ptr(q_idx), _ptr(q_val), _ptr(k_idx), _ptr(k_val), _ptr(v), _ptr(sel), nsel,
+                              _ptr(o), _ptr(lse), int(threads))
+    if st:
+        raise OracleError(st)
+    return o, lse
+
+
+def scores_row(q_idx, q_val, k_idx, k_val, flat_row, *, d, causal=True, scale=None, q_pos0=0):
+    q_idx = np.ascontiguousarray(q_idx); q_val = np.ascontiguousarray(q_val)
+    k_idx = np.ascontiguousarray(k_idx); k_val = np.ascontiguousarray(k_val)
+    B, H, n_q, k = q_idx.shape
+    _, H_kv, n_kv, _ = k_idx.shape
+    if scale is None:
+        scale = 1.0 / np.sqrt(d)
+    s = np.zeros((n_kv,), np.float64)
+    st = _load().ref_scores_row(B, H, H_kv, d, k, n_q, n_kv, q_pos0, int(bool(causal)), float(scale),
+                                _dtype_code(q_val), _ptr(q_idx), _ptr(q_val), _ptr(k_idx), _ptr(k_val),
+                                int(flat_row), _ptr(s))
+    if st:
+        raise OracleError(st)
+    return s
+
+
+def edge_count(q_idx, k_idx, *, causal=True, q_pos0=0) -> int:
+    q_idx = np.ascontiguousarray(q_idx); k_idx = np.ascontiguousarray(k_idx)
+    B, H, n_q, k = q_idx.shape
+    _, H_kv, n_kv, _ = k_idx.shape
+    return int(_load().ref_edge_count(B, H, H_kv, k, n_q, n_kv, q_pos0, int(bool(causal)),
+                                      _ptr(q_idx), _ptr(k_idx)))
