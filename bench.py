@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""FlashSFA forward benchmark (the driver's contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config qwen3] [--kernel auto|simt|sm100]
+    python bench.py --impl reference ...      # the fp64 CPU oracle on this box's host cores
+
+One step = one pass of the whole hot path over one batch element of the
+workload: top-k codes of Q and of K (stage 1), key-tile bucketing, FlashSFA attention (stage 2),
+inputs resident in HBM.  Weak scaling: rank r owns batch element r of a B=N batch (independent
+problems, no data-path collective).  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2603_22300_b200 import accounting  # noqa: E402
+
+METRIC = "FlashSFA fwd ms & tokens/s at n=32K,d=128,k=16; HBM GB/s vs peak; 1/2/4/8 GPU"
+L2_BYTES = 126 * 2 ** 20
+MUFU_EX2_PER_CLK_SM = 16  # B200 SFU ex2 rate (sm_100; the B300 guide's 2x SFU is sm_103-only)
+N_SMS = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="qwen3", choices=sorted(accounting.CONFIGS))
+    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "sm100"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--k", type=int, default=None, help="override the code size k (sweep)")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return dict(hbm_gbs=d["hbm_gbs"], bf16_tflops=d["bf16_tflops"], sm_max_mhz=d.get("sm_max_mhz", 1965.0),
+                    source="measured (MEASURED_PEAKS.json)")
+    return dict(hbm_gbs=6650.0, bf16_tflops=1590.0, sm_max_mhz=1965.0, source="fallback (B200_PROFILING.md)")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 9 for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------------------------
+# CPU oracle (cpu_baseline leg and --impl reference): the oracle as it stands, on a bounded sample
+# --------------------------------------------------------------------------------------------
+def oracle_sample(W, seed, n_rows, n_topk_rows, threads):
+    """Time the oracle on a bounded sample of the workload, extrapolated to tokens/s.
+
+    Sample: top-k of n_topk_rows Q rows and n_topk_rows K rows, plus the attention of n_rows
+    uniformly random (head, position) query rows over all of their allowed keys (the causal
+    row cost is linear in the position, so a uniform sample is unbiased)."""
+    import numpy as np
+
+    import oracle
+    from paper_2603_22300_b200 import inputs
+    rng = np.random.default_rng(seed)
+    B, H, H_kv, n, d, d_v, k = 1, W.H, W.H_kv, W.n, W.d, W.d_v, W.k
+    # inputs for the sample (generation is not timed)
+    kx = inputs.gen(seed, inputs.TID_K, (B, H_kv, n, d), W.dtype)
+    v = inputs.gen(seed, inputs.TID_V, (B, H_kv, n, d_v), W.dtype)
+    rows = np.sort(rng.choice(B * H * n, n_rows, replace=False)).astype(np.int64)
+    qflat = rows[:, None] * d + np.arange(d)[None, :]
+    q_rows = inputs.gen(seed, inputs.TID_Q, (B, H, n, d), W.dtype, flat=qflat)
+    q_top = inputs.gen(seed, inputs.TID_Q, (n_topk_rows, d), W.dtype)
+    # --- timed: top-k sample
+    t0 = time.perf_counter()
+    oracle.topk_codes(q_top, k)
+    oracle.topk_codes(kx.reshape(-1, d)[:n_topk_rows], k)
+    t_topk = time.perf_counter() - t0
+    # codes the attention sample needs (all keys of the kv heads, the sampled query rows): untimed
+    ki, kv = oracle.topk_codes(kx.reshape(-1, d), k)
+    qi_r, qv_r = oracle.topk_codes(q_rows, k)
+    qi = np.zeros((B, H, n, k), np.uint8)
+    qv = np.zeros((B, H, n, k), qv_r.dtype)
+    qi.reshape(-1, k)[rows] = qi_r
+    qv.reshape(-1, k)[rows] = qv_r
+    t0 = time.perf_counter()
+    oracle.attn_fwd(qi, qv, ki.reshape(B, H_kv, n, k), kv.reshape(B, H_kv, n, k), v, d=d, rows=rows,
+                    threads=threads)
+    t_attn = time.perf_counter() - t0
+    total_rows_q = B * H * n
+    total_rows_topk = B * (H + H_kv) * n
+    t_full = t_attn * total_rows_q / n_rows + t_topk * total_rows_topk / (2 * n_topk_rows)
+    return {"tokens_per_s": B * n / t_full, "t_sample": t_topk + t_attn, "t_full_extrapolated": t_full,
+            "sample": f"{n_rows} uniformly random (head, position) query rows of the {W.H}x{W.n} grid over all "
+                      f"their allowed keys + top-k of {n_topk_rows} Q and {n_topk_rows} K rows; "
+                      f"linear extrapolation to the full {B}x{H}x{n} workload"}
+
+
+def run_reference(args, W, rank):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    # size each step so warmup+steps finish in about 2-3 minutes on this host
+    budget_s = 150.0 / max(1, args.steps + args.warmup)
+    n_rows = 64
+    probe = oracle_sample(W, 7, n_rows, 256, threads)
+    per_row = probe["t_sample"] / n_rows
+    n_rows = int(max(16, min(4096, budget_s / max(per_row, 1e-6))))
+    for i in range(args.warmup):
+        oracle_sample(W, 100 + i, n_rows, 256, threads)
+    vals, ts = [], []
+    for i in range(args.steps):
+        r = oracle_sample(W, 200 + i, n_rows, 256, threads)
+        vals.append(r["tokens_per_s"])
+        ts.append(r["t_full_extrapolated"])
+    value = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(ts),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded counter-based generator, DESIGN.md input recipe)",
+            "config": config_of(args, W),
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+                             "sample": r["sample"]},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_of(args, W):
+    return {"workload": f"{args.config}: B={W.B} per GPU, H={W.H}, H_kv={W.H_kv}, n={W.n}, d={W.d}, d_v={W.d_v}, "
+                        f"k={W.k}, {'causal' if W.causal else 'non-causal'}, {W.dtype} V",
+            "global_batch": W.B * args.gpus, "seq_len": W.n, "parallelism": f"weak: batch element r on rank r "
+            f"({args.gpus} GPU{'s' if args.gpus > 1 else ''}), no data-path collective",
+            "kernel": args.kernel,
+            "l2": f"explicit {L2_FLUSH_MB} MB write between timed steps (outside the step events); "
+                  "inputs+outputs also exceed the 126 MB L2"}
+
+
+L2_FLUSH_MB = 512
+
+
+# --------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    W = accounting.CONFIGS[args.config]
+    if args.k is not None:
+        W = accounting.Workload(**{**W.__dict__, "k": args.k})
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, W, rank)
+        return
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_22300_b200 import inputs, sfa
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    kernel = {"auto": sfa.KERNEL_AUTO, "simt": sfa.KERNEL_SIMT, "sm100": sfa.KERNEL_SM100}[args.kernel]
+    dt = torch.bfloat16 if W.dtype == "bf16" else torch.float32
+    seed = accounting.SEEDS[args.config]
+    B, H, H_kv, n, d, d_v, k = W.B, W.H, W.H_kv, W.n, W.d, W.d_v, W.k
+    dev = torch.device("cuda", local)
+    # rank r holds batch element r of the global B = world batch: offset into the generator stream
+    Q = torch.empty((B, H, n, d), dtype=dt, device=dev)
+    K = torch.empty((B, H_kv, n, d), dtype=dt, device=dev)
+    V = torch.empty((B, H_kv, n, d_v), dtype=dt, device=dev)
+    sfa.gen_fill(Q, seed, inputs.TID_Q, offset=rank * Q.numel())
+    sfa.gen_fill(K, seed, inputs.TID_K, offset=rank * K.numel())
+    sfa.gen_fill(V, seed, inputs.TID_V, offset=rank * V.numel())
+    desc = sfa.make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k, d_v=d_v, n_q=n, n_kv=n, causal=W.causal,
+                         dtype=sfa.SFA_BF16 if W.dtype == "bf16" else sfa.SFA_F32, kernel=kernel)
+    q_idx = torch.empty((B, H, n, k), dtype=torch.uint8, device=dev)
+    q_val = torch.empty((B, H, n, k), dtype=dt, device=dev)
+    k_idx = torch.empty((B, H_kv, n, k), dtype=torch.uint8, device=dev)
+    k_val = torch.empty((B, H_kv, n, k), dtype=dt, device=dev)
+    ws = torch.empty(sfa.workspace_bytes(desc), dtype=torch.uint8, device=dev)
+    O = torch.empty((B, H, n, d_v), dtype=dt, device=dev)
+    LSE = torch.empty((B, H, n), dtype=torch.float32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    flush = torch.empty(L2_FLUSH_MB * 2 ** 20, dtype=torch.uint8, device=dev)
+    L = sfa.lib()
+    import ctypes
+    st = lambda: ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    P = lambda t: ctypes.c_void_p(t.data_ptr())
+    dcode = desc.dtype
+
+    def step(ev=None):
+        # stage 1 on Q, stage 1 on K, step 3 bucketing, steps 4-8 attention -- 4 launches of ours
+        if ev: ev[0].record()
+        r1 = L.sfa_topk_codes(P(Q), dcode, B * H * n, d, d, k, P(q_idx), P(q_val), P(status), st())
+        if ev: ev[1].record()
+        r2 = L.sfa_topk_codes(P(K), dcode, B * H_kv * n, d, d, k, P(k_idx), P(k_val), P(status), st())
+        if ev: ev[2].record()
+        r3 = L.sfa_bucket_keys(ctypes.byref(desc), P(k_idx), P(k_val), P(ws), ws.numel(), st())
+        if ev: ev[3].record()
+        r4 = L.sfa_attn_fwd_bucketed(ctypes.byref(desc), P(q_idx), P(q_val), P(V), P(O), P(LSE), P(ws), ws.numel(),
+                                     st())
+        if ev: ev[4].record()
+        if r1 or r2 or r3 or r4:
+            raise RuntimeError(f"sfa call failed: {(r1, r2, r3, r4)}")
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_wall0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush: outside the step's events
+            step(evs[i])
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+    if world > 1:
+        dist.barrier()
+    per = [[e[j].elapsed_time(e[j + 1]) for j in range(4)] for e in evs]  # ms per stage per step
+    step_ms = [sum(p) for p in per]
+    tot_ms = sum(step_ms)
+    stage_ms = [sum(p[j] for p in per) / args.steps for j in range(4)]
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ms_per_step = tot_ms / args.steps
+    tokens_per_step = B * n * world
+    value = tokens_per_step / (ms_per_step / 1e3)
+    torch.cuda.synchronize()
+    if int(status.item()) != 0:
+        raise RuntimeError("non-finite inputs flagged")
+
+    # ---- end to end through the C ABI with HOST buffers (copies inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        qh = Q.cpu().pin_memory(); kh = K.cpu().pin_memory(); vh = V.cpu().pin_memory()
+        oh = torch.empty(O.shape, dtype=dt).pin_memory()
+        lh = torch.empty(LSE.shape, dtype=torch.float32).pin_memory()
+        scratch = torch.empty(sfa.scratch_bytes(desc), dtype=torch.uint8, device=dev)
+        bufs = (torch.empty_like(Q), torch.empty_like(K), torch.empty_like(V), torch.empty_like(O),
+                torch.empty_like(LSE))
+        for _ in range(max(1, args.warmup)):
+            sfa.forward_host(desc, qh, kh, vh, oh, lh, bufs, scratch)
+        e2e_steps = max(1, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(e2e_steps):
+            sfa.forward_host(desc, qh, kh, vh, oh, lh, bufs, scratch)
+        e1.record()
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1) / e2e_steps
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        h2d = (Q.numel() + K.numel() + V.numel()) * Q.element_size()
+        d2h = O.numel() * O.element_size() + LSE.numel() * 4 + 4
+        e2e = {"value": tokens_per_step / (e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "api": "sfa_forward_host (pinned host q,k,v -> o,lse; stream-synchronised)"}
+        del qh, kh, vh, oh, lh, scratch, bufs
+
+    pk = peaks()
+    attn_ms = stage_ms[3]
+    pairs = B * H * accounting.causal_pairs(n, n, 0, W.causal)
+    mufu_peak = N_SMS * MUFU_EX2_PER_CLK_SM * pk["sm_max_mhz"] * 1e6  # ex2/s
+    achieved = pairs / (attn_ms / 1e3)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(args.config, {}).get(f"attn_{args.kernel}")
+        except Exception:
+            traffic = None
+    topk_bytes = W.topk_bytes()
+    roofline = {"bound": "alu", "kernel": "sfa attention (steps 4-8)", "achieved": achieved / 1e9,
+                "peak": mufu_peak / 1e9, "unit": "G pairs/s (1 MUFU ex2 per allowed pair)",
+                "frac": achieved / mufu_peak, "traffic": traffic,
+                "peak_source": f"148 SMs x 16 ex2/clk x {pk['sm_max_mhz']:.0f} MHz (DESIGN.md)",
+                "other_floors": {
+                    "tensor_pv_frac": (2.0 * d_v * pairs / (attn_ms / 1e3)) / (pk["bf16_tflops"] * 1e12),
+                    "hbm_attn_frac": (W.attn_min_bytes() / (attn_ms / 1e3)) / (pk["hbm_gbs"] * 1e9),
+                    "topk_hbm_gbs": topk_bytes / ((stage_ms[0] + stage_ms[1]) / 1e3) / 1e9,
+                    "topk_hbm_frac": topk_bytes / ((stage_ms[0] + stage_ms[1]) / 1e3) / (pk["hbm_gbs"] * 1e9),
+                    "peaks": pk["source"]}}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        r = oracle_sample(W, seed, 1024, 2048, threads)
+        cpu = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": threads, "kind": "oracle",
+               "sample": r["sample"], "sample_seconds": r["t_sample"]}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": W.dtype,
+                "data": "synthetic (seeded counter-based generator on device, DESIGN.md input recipe)",
+                "config": config_of(args, W),
+                "stage_ms": {"topk_q": stage_ms[0], "topk_k": stage_ms[1], "bucket": stage_ms[2],
+                             "attn": stage_ms[3]},
+                "interactions_per_s": W.expected_interactions / (ms_per_step / 1e3) * world,
+                "pairs_per_s": pairs * world / (ms_per_step / 1e3),
+                "wall_s_timed_region": t_wall,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 4 * args.steps,
+                "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,146 @@
+/*
+ * include/sfa.h -- C ABI of the B200 (sm_100a) FlashSFA hot path.
+ *
+ * Sparse Feature Attention (arXiv 2603.22300).  Citations: "P:Lnnn" = PAPER.md line nnn,
+ * "S:Lnnn" = SPEC.md line nnn; readings A1..A21 are listed in DESIGN.md.
+ *
+ * The path has two stages:
+ *   stage 1  sfa_topk_codes  -- row-wise Top-k coding of Q and of K (Eq. topk_QK):
+ *            keep the k entries of largest |x|, sign kept; ties -> lower index (A2);
+ *            indices ascending (A4); always exactly k entries (A8).
+ *   stage 2  sfa_attn_fwd    -- the exact attention forward over those codes (P:L97-101 Eq. s_ij,
+ *            P:L126-135 Sec. 3.2, Alg. 1):
+ *              s_ij = scale * sum_{u in S_i and S_j} q~_iu k~_ju   (0 when disjoint: A1/R1)
+ *              O_i  = sum_j softmax_j(s_ij, j allowed) V_j ;  LSE_i = ln sum_j exp(s_ij)  (A11)
+ *            computed tile by tile with an online softmax; no n x n matrix is ever stored.
+ *
+ * Conventions for every call:
+ *   - Tensor pointers are DEVICE pointers owned by the caller (the Python layer allocates them
+ *     with PyTorch), except in sfa_forward_host, whose inputs/outputs are HOST pointers.
+ *   - The library never allocates device memory, never frees, never synchronises the device
+ *     (sfa_forward_host synchronises its stream), and keeps no mutable global state: calls are
+ *     thread-safe and ordered on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *   - Argument errors are detected on the host BEFORE any launch and leave outputs untouched.
+ *   - Data errors (non-finite inputs) are reported asynchronously through `status_word`.
+ *   - All tensors are dense, row-major, last index fastest, 16-byte aligned.
+ */
+#ifndef SFA_H
+#define SFA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SFA_API __attribute__((visibility("default")))
+#else
+#define SFA_API
+#endif
+
+typedef struct CUstream_st *sfa_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    SFA_OK = 0,
+    SFA_ERR_INVALID_ARGUMENT = 1, /* bad shape / k / scale / null or misaligned pointer */
+    SFA_ERR_INVALID_INPUT = 2,    /* non-finite input values (reading A14)                      */
+    SFA_ERR_UNSUPPORTED = 3,      /* valid but not compiled (d, d_v not in {64,128}), or no sm_100 GPU */
+    SFA_ERR_RESOURCE = 4,         /* workspace / scratch too small (S:L180 resource-limit)             */
+    SFA_ERR_CUDA = 5              /* a CUDA launch or copy failed                                      */
+} sfa_status;
+
+typedef enum { SFA_F32 = 0, SFA_BF16 = 1 } sfa_dtype;
+
+/* Kernel selection for sfa_attn_fwd (desc.kernel). */
+typedef enum {
+    SFA_KERNEL_AUTO = 0, /* the fastest kernel compiled for the shape                               */
+    SFA_KERNEL_SIMT = 1, /* CUDA-core kernel: bucket scatter + FFMA P.V (the only fp32 P.V path: A12) */
+    SFA_KERNEL_SM100 = 2 /* sm_100a kernel: bucket scatter + tcgen05 P.V, O and P in TMEM (bf16 only) */
+} sfa_kernel;
+
+SFA_API const char *sfa_status_string(sfa_status s);
+
+/* ------------------------------------------------------------------------------------------
+ * Stage 1: Top-k codes.
+ *   x    [rows][d] with row stride `ld` elements (ld >= d); dtype SFA_F32 or SFA_BF16.
+ *        rows = B*H*n for Q, B*H_kv*n for K (the same operator on Q and on K).
+ *   idx  [rows][k] uint8, ascending feature indices (A4, A6: u8 covers d <= 256).
+ *   val  [rows][k] same dtype as x, bit copies of the selected entries (A7; -0 kept).
+ *   Ranking key |x| compared exactly (IEEE magnitude bits; no flush-to-zero, A21); ties -> lower index.
+ *   status_word (nullable, device): bit 0 is OR-ed in when any non-finite x is seen; the outputs
+ *        are then unspecified and the caller reports SFA_ERR_INVALID_INPUT (A14).
+ *   Requires 1 <= k <= d, d in {64, 128}, rows >= 0.  Stream-ordered, no allocation.
+ * ------------------------------------------------------------------------------------------ */
+SFA_API sfa_status sfa_topk_codes(const void *x, sfa_dtype dtype, int64_t rows, int32_t d, int64_t ld, int32_t k,
+                          uint8_t *idx, void *val, uint32_t *status_word, sfa_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Stage 2: attention forward over the codes.
+ * ------------------------------------------------------------------------------------------ */
+typedef struct {
+    int32_t B, H, H_kv;  /* batch, query heads, kv heads; H % H_kv == 0; head h reads kv head h/(H/H_kv) (A15) */
+    int32_t d, k, d_v;   /* head dim (64|128), code size (1..d), value dim (64|128)                       */
+    int64_t n_q, n_kv;   /* query rows and keys per head (n_q >= 1, n_kv >= 1)                             */
+    int64_t q_pos0;      /* query i sits at global position q_pos0 + i (A9); >= 0                          */
+    int32_t causal;      /* 1: key j allowed iff j <= q_pos0 + i ("masking for causality"); 0: all */
+    float scale;         /* logit multiplier; > 0 and finite; the paper's is 1/sqrt(d) (A5)         */
+    sfa_dtype dtype;     /* dtype of q_val, k_val, v and o (LSE is always fp32)                            */
+    int32_t kernel;      /* sfa_kernel; SFA_KERNEL_AUTO unless benchmarking an ablation                   */
+} sfa_attn_desc;
+
+/* Bytes of device workspace sfa_attn_fwd needs: the key-tile feature buckets (DESIGN.md
+ * "Key-tile bucketing", our form of the paper's CSC_feat). 0 on invalid desc. */
+SFA_API size_t sfa_attn_workspace_bytes(const sfa_attn_desc *desc);
+
+/* O, LSE = FlashSFA forward.
+ *   q_idx [B][H][n_q][k] u8,  q_val [B][H][n_q][k]   (stage-1 codes of Q)
+ *   k_idx [B][H_kv][n_kv][k] u8, k_val [B][H_kv][n_kv][k]
+ *   v     [B][H_kv][n_kv][d_v]       o [B][H][n_q][d_v] (dtype)       lse [B][H][n_q] fp32, natural log
+ *   workspace: >= sfa_attn_workspace_bytes(desc) device bytes (else SFA_ERR_RESOURCE).
+ *   Launches the bucketing kernel and the attention kernel on `stream`.
+ *   O is rounded to the output dtype with round-to-nearest-even (A21). Rows with no allowed key
+ *   (impossible when q_pos0 >= 0) get O = 0, LSE = -inf (A10). */
+SFA_API sfa_status sfa_attn_fwd(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val, const uint8_t *k_idx,
+                        const void *k_val, const void *v, void *o, float *lse, void *workspace,
+                        size_t workspace_bytes, sfa_stream_t stream);
+
+/* Step 3 alone (exposed for tests and for the sharded path, which buckets the gathered keys once):
+ * builds the buckets of every key tile into `workspace` (layout in DESIGN.md).  sfa_attn_fwd calls it. */
+SFA_API sfa_status sfa_bucket_keys(const sfa_attn_desc *desc, const uint8_t *k_idx, const void *k_val, void *workspace,
+                           size_t workspace_bytes, sfa_stream_t stream);
+
+/* Attention over buckets already built by sfa_bucket_keys (same desc, same workspace). */
+SFA_API sfa_status sfa_attn_fwd_bucketed(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val,
+                                 const void *v, void *o, float *lse, const void *workspace,
+                                 size_t workspace_bytes, sfa_stream_t stream);
+
+/* Key tile size the bucket layout and kernels use for this desc (128, or 64 when k > 32). */
+SFA_API int32_t sfa_key_tile(const sfa_attn_desc *desc);
+
+/* ------------------------------------------------------------------------------------------
+ * The whole hot path in one call: codes of Q and K (stage 1) then the attention (stage 2).
+ *   q [B][H][n_q][d], k [B][H_kv][n_kv][d], v [B][H_kv][n_kv][d_v], o, lse as above.
+ *   scratch: >= sfa_forward_scratch_bytes(desc) device bytes; holds the codes, buckets and
+ *   the status word.  Non-finite q/k are detected asynchronously (status word in scratch;
+ *   sfa_forward_host checks it and returns SFA_ERR_INVALID_INPUT).
+ * ------------------------------------------------------------------------------------------ */
+SFA_API size_t sfa_forward_scratch_bytes(const sfa_attn_desc *desc);
+SFA_API sfa_status sfa_forward(const sfa_attn_desc *desc, const void *q, const void *k, const void *v, void *o, float *lse,
+                       void *scratch, size_t scratch_bytes, sfa_stream_t stream);
+
+/* Same, end to end from HOST buffers: copies q, k, v (pinned host memory recommended) into the
+ * caller's device buffers q_dev/k_dev/v_dev, runs sfa_forward, copies o and lse back into
+ * o_host/lse_host, and synchronises `stream` before returning (so the host outputs are valid). */
+SFA_API sfa_status sfa_forward_host(const sfa_attn_desc *desc, const void *q_host, const void *k_host, const void *v_host,
+                            void *o_host, float *lse_host, void *q_dev, void *k_dev, void *v_dev, void *o_dev,
+                            float *lse_dev, void *scratch, size_t scratch_bytes, sfa_stream_t stream);
+
+/* Build / device info: 1 if the calling thread's current device is sm_100 and the kernels load. */
+SFA_API int32_t sfa_device_supported(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SFA_H */

@@ -1,0 +1,234 @@
+// api.cu -- the C ABI (include/sfa.h): host-side validation, workspace layout, kernel selection.
+// Every argument check runs before any launch, so a rejected call leaves all outputs untouched.
+#include <math.h>
+#include <string.h>
+
+#include "../../include/sfa.h"
+#include "launch.cuh"
+
+using namespace sfa;
+
+namespace {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+sfa_status from_cuda(cudaError_t e) { return e == cudaSuccess ? SFA_OK : SFA_ERR_CUDA; }
+
+int key_tile(int k) { return k <= 32 ? 128 : 64; }
+
+sfa_status validate_desc(const sfa_attn_desc *d) {
+    if (!d) return SFA_ERR_INVALID_ARGUMENT;
+    if (d->B < 1 || d->H < 1 || d->H_kv < 1 || d->H % d->H_kv) return SFA_ERR_INVALID_ARGUMENT;
+    if (d->d < 1 || d->d > 256 || d->k < 1 || d->k > d->d || d->d_v < 1) return SFA_ERR_INVALID_ARGUMENT;
+    if (d->n_q < 1 || d->n_kv < 1 || d->q_pos0 < 0) return SFA_ERR_INVALID_ARGUMENT;
+    if (d->causal != 0 && d->causal != 1) return SFA_ERR_INVALID_ARGUMENT;
+    if (!(d->scale > 0.f) || !isfinite(d->scale)) return SFA_ERR_INVALID_ARGUMENT;
+    if (d->dtype != SFA_F32 && d->dtype != SFA_BF16) return SFA_ERR_INVALID_ARGUMENT;
+    if (d->kernel < SFA_KERNEL_AUTO || d->kernel > SFA_KERNEL_SM100) return SFA_ERR_INVALID_ARGUMENT;
+    if (d->d != 64 && d->d != 128) return SFA_ERR_UNSUPPORTED;
+    if (d->d_v != 64 && d->d_v != 128) return SFA_ERR_UNSUPPORTED;
+    if (d->kernel == SFA_KERNEL_SM100 && d->dtype != SFA_BF16) return SFA_ERR_UNSUPPORTED;
+    if ((d->n_kv + 63) / 64 > (int64_t)INT32_MAX) return SFA_ERR_UNSUPPORTED;
+    return SFA_OK;
+}
+
+BucketLayout layout_of(const sfa_attn_desc *d) {
+    return make_layout(d->d, d->k, d->n_kv, key_tile(d->k), d->dtype == SFA_BF16);
+}
+
+size_t ws_bytes(const sfa_attn_desc *d) {
+    const BucketLayout L = layout_of(d);
+    return (size_t)d->B * d->H_kv * L.ntiles * L.tile_bytes;
+}
+
+size_t esize(sfa_dtype t) { return t == SFA_BF16 ? 2 : 4; }
+
+// scratch of sfa_forward: [status 256 B][q_idx][q_val][k_idx][k_val][buckets], each 256-aligned
+struct Scratch {
+    size_t status, q_idx, q_val, k_idx, k_val, ws, total;
+};
+Scratch scratch_layout(const sfa_attn_desc *d) {
+    Scratch s;
+    const size_t rq = (size_t)d->B * d->H * d->n_q, rk = (size_t)d->B * d->H_kv * d->n_kv;
+    size_t o = 0;
+    s.status = o; o += 256;
+    s.q_idx = o; o += align_up(rq * d->k, 256);
+    s.q_val = o; o += align_up(rq * d->k * esize(d->dtype), 256);
+    s.k_idx = o; o += align_up(rk * d->k, 256);
+    s.k_val = o; o += align_up(rk * d->k * esize(d->dtype), 256);
+    s.ws = o; o += align_up(ws_bytes(d), 256);
+    s.total = o;
+    return s;
+}
+
+sfa_status run_attn(const sfa_attn_desc *d, const uint8_t *q_idx, const void *q_val, const void *v, void *o,
+                    float *lse, const void *ws, cudaStream_t st) {
+    AttnParams p;
+    p.q_idx = q_idx; p.q_val = q_val; p.v = v; p.o = o; p.lse = lse; p.ws = (const uint8_t *)ws;
+    p.B = d->B; p.H = d->H; p.H_kv = d->H_kv; p.k = d->k;
+    p.n_q = d->n_q; p.n_kv = d->n_kv; p.q_pos0 = d->q_pos0; p.causal = d->causal;
+    p.scale_log2 = d->scale * kLog2e;
+    p.L = layout_of(d);
+    const bool bf16 = d->dtype == SFA_BF16;
+    if (bf16 && d->kernel != SFA_KERNEL_SIMT) {
+        cudaError_t e = launch_attn_sm100(p, d->d, d->d_v, st);
+        if (e == cudaSuccess) return SFA_OK;
+        if (e != cudaErrorNotSupported || d->kernel == SFA_KERNEL_SM100) return e == cudaErrorNotSupported ? SFA_ERR_UNSUPPORTED : SFA_ERR_CUDA;
+        (void)cudaGetLastError();
+    }
+    return from_cuda(launch_attn_simt(p, bf16, d->d, d->d_v, st));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *sfa_status_string(sfa_status s) {
+    switch (s) {
+        case SFA_OK: return "ok";
+        case SFA_ERR_INVALID_ARGUMENT: return "invalid-argument";
+        case SFA_ERR_INVALID_INPUT: return "invalid-input";
+        case SFA_ERR_UNSUPPORTED: return "unsupported";
+        case SFA_ERR_RESOURCE: return "resource-limit";
+        case SFA_ERR_CUDA: return "cuda-error";
+    }
+    return "unknown-status";
+}
+
+sfa_status sfa_topk_codes(const void *x, sfa_dtype dtype, int64_t rows, int32_t d, int64_t ld, int32_t k,
+                          uint8_t *idx, void *val, uint32_t *status_word, sfa_stream_t stream) {
+    if (dtype != SFA_F32 && dtype != SFA_BF16) return SFA_ERR_INVALID_ARGUMENT;
+    if (rows < 0 || d < 1 || d > 256 || k < 1 || k > d || ld < d) return SFA_ERR_INVALID_ARGUMENT;
+    if (d != 64 && d != 128) return SFA_ERR_UNSUPPORTED;
+    if (rows == 0) return SFA_OK;
+    if (!x || !idx || !val) return SFA_ERR_INVALID_ARGUMENT;
+    // every lane issues one vector load of d/32 elements: the row starts must be vector aligned
+    const size_t vec = (size_t)(d / 32) * esize(dtype);
+    if (((uintptr_t)x % vec) || ((size_t)ld * esize(dtype)) % vec) return SFA_ERR_INVALID_ARGUMENT;
+    if (status_word && ((uintptr_t)status_word & 3u)) return SFA_ERR_INVALID_ARGUMENT;
+    return from_cuda(launch_topk(x, dtype == SFA_BF16, rows, d, ld, k, idx, val, status_word, (cudaStream_t)stream));
+}
+
+size_t sfa_attn_workspace_bytes(const sfa_attn_desc *desc) {
+    if (validate_desc(desc) != SFA_OK) return 0;
+    return ws_bytes(desc);
+}
+
+int32_t sfa_key_tile(const sfa_attn_desc *desc) {
+    if (validate_desc(desc) != SFA_OK) return 0;
+    return key_tile(desc->k);
+}
+
+sfa_status sfa_bucket_keys(const sfa_attn_desc *desc, const uint8_t *k_idx, const void *k_val, void *workspace,
+                           size_t workspace_bytes, sfa_stream_t stream) {
+    sfa_status s = validate_desc(desc);
+    if (s != SFA_OK) return s;
+    if (!k_idx || !k_val || !workspace || !aligned16(workspace)) return SFA_ERR_INVALID_ARGUMENT;
+    if (workspace_bytes < ws_bytes(desc)) return SFA_ERR_RESOURCE;
+    return from_cuda(launch_bucket(k_idx, k_val, desc->dtype == SFA_BF16, desc->d, desc->k,
+                                   (int64_t)desc->B * desc->H_kv, desc->n_kv, layout_of(desc), workspace,
+                                   (cudaStream_t)stream));
+}
+
+sfa_status sfa_attn_fwd_bucketed(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val, const void *v,
+                                 void *o, float *lse, const void *workspace, size_t workspace_bytes,
+                                 sfa_stream_t stream) {
+    sfa_status s = validate_desc(desc);
+    if (s != SFA_OK) return s;
+    if (!q_idx || !q_val || !v || !o || !lse || !workspace) return SFA_ERR_INVALID_ARGUMENT;
+    if (!aligned16(v) || !aligned16(o) || !aligned16(workspace) || ((uintptr_t)lse & 3u))
+        return SFA_ERR_INVALID_ARGUMENT;
+    if (workspace_bytes < ws_bytes(desc)) return SFA_ERR_RESOURCE;
+    return run_attn(desc, q_idx, q_val, v, o, lse, workspace, (cudaStream_t)stream);
+}
+
+sfa_status sfa_attn_fwd(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val, const uint8_t *k_idx,
+                        const void *k_val, const void *v, void *o, float *lse, void *workspace,
+                        size_t workspace_bytes, sfa_stream_t stream) {
+    sfa_status s = validate_desc(desc);
+    if (s != SFA_OK) return s;
+    if (!q_idx || !q_val || !k_idx || !k_val || !v || !o || !lse || !workspace) return SFA_ERR_INVALID_ARGUMENT;
+    if (!aligned16(v) || !aligned16(o) || !aligned16(workspace) || ((uintptr_t)lse & 3u))
+        return SFA_ERR_INVALID_ARGUMENT;
+    if (workspace_bytes < ws_bytes(desc)) return SFA_ERR_RESOURCE;
+    s = from_cuda(launch_bucket(k_idx, k_val, desc->dtype == SFA_BF16, desc->d, desc->k,
+                                (int64_t)desc->B * desc->H_kv, desc->n_kv, layout_of(desc), workspace,
+                                (cudaStream_t)stream));
+    if (s != SFA_OK) return s;
+    return run_attn(desc, q_idx, q_val, v, o, lse, workspace, (cudaStream_t)stream);
+}
+
+size_t sfa_forward_scratch_bytes(const sfa_attn_desc *desc) {
+    if (validate_desc(desc) != SFA_OK) return 0;
+    return scratch_layout(desc).total;
+}
+
+sfa_status sfa_forward(const sfa_attn_desc *desc, const void *q, const void *k, const void *v, void *o, float *lse,
+                       void *scratch, size_t scratch_bytes, sfa_stream_t stream) {
+    sfa_status s = validate_desc(desc);
+    if (s != SFA_OK) return s;
+    if (!q || !k || !v || !o || !lse || !scratch) return SFA_ERR_INVALID_ARGUMENT;
+    if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o) || !aligned16(scratch) ||
+        ((uintptr_t)lse & 3u))
+        return SFA_ERR_INVALID_ARGUMENT;
+    const Scratch L = scratch_layout(desc);
+    if (scratch_bytes < L.total) return SFA_ERR_RESOURCE;
+    uint8_t *S = (uint8_t *)scratch;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint32_t *status = (uint32_t *)(S + L.status);
+    cudaError_t e = cudaMemsetAsync(status, 0, 4, st);
+    if (e != cudaSuccess) return SFA_ERR_CUDA;
+    const bool bf16 = desc->dtype == SFA_BF16;
+    e = launch_topk(q, bf16, (int64_t)desc->B * desc->H * desc->n_q, desc->d, desc->d, desc->k, S + L.q_idx,
+                    S + L.q_val, status, st);
+    if (e != cudaSuccess) return SFA_ERR_CUDA;
+    e = launch_topk(k, bf16, (int64_t)desc->B * desc->H_kv * desc->n_kv, desc->d, desc->d, desc->k, S + L.k_idx,
+                    S + L.k_val, status, st);
+    if (e != cudaSuccess) return SFA_ERR_CUDA;
+    e = launch_bucket(S + L.k_idx, S + L.k_val, bf16, desc->d, desc->k, (int64_t)desc->B * desc->H_kv, desc->n_kv,
+                      layout_of(desc), S + L.ws, st);
+    if (e != cudaSuccess) return SFA_ERR_CUDA;
+    return run_attn(desc, S + L.q_idx, S + L.q_val, v, o, lse, S + L.ws, st);
+}
+
+sfa_status sfa_forward_host(const sfa_attn_desc *desc, const void *q_host, const void *k_host, const void *v_host,
+                            void *o_host, float *lse_host, void *q_dev, void *k_dev, void *v_dev, void *o_dev,
+                            float *lse_dev, void *scratch, size_t scratch_bytes, sfa_stream_t stream) {
+    sfa_status s = validate_desc(desc);
+    if (s != SFA_OK) return s;
+    if (!q_host || !k_host || !v_host || !o_host || !lse_host) return SFA_ERR_INVALID_ARGUMENT;
+    if (!q_dev || !k_dev || !v_dev || !o_dev || !lse_dev || !scratch) return SFA_ERR_INVALID_ARGUMENT;
+    const Scratch L = scratch_layout(desc);
+    if (scratch_bytes < L.total) return SFA_ERR_RESOURCE;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t es = esize(desc->dtype);
+    const size_t qb = (size_t)desc->B * desc->H * desc->n_q * desc->d * es;
+    const size_t kb = (size_t)desc->B * desc->H_kv * desc->n_kv * desc->d * es;
+    const size_t vb = (size_t)desc->B * desc->H_kv * desc->n_kv * desc->d_v * es;
+    const size_t ob = (size_t)desc->B * desc->H * desc->n_q * desc->d_v * es;
+    const size_t lb = (size_t)desc->B * desc->H * desc->n_q * 4;
+    if (cudaMemcpyAsync(q_dev, q_host, qb, cudaMemcpyHostToDevice, st) != cudaSuccess) return SFA_ERR_CUDA;
+    if (cudaMemcpyAsync(k_dev, k_host, kb, cudaMemcpyHostToDevice, st) != cudaSuccess) return SFA_ERR_CUDA;
+    if (cudaMemcpyAsync(v_dev, v_host, vb, cudaMemcpyHostToDevice, st) != cudaSuccess) return SFA_ERR_CUDA;
+    s = sfa_forward(desc, q_dev, k_dev, v_dev, o_dev, lse_dev, scratch, scratch_bytes, stream);
+    if (s != SFA_OK) return s;
+    uint32_t status = 0;
+    if (cudaMemcpyAsync(o_host, o_dev, ob, cudaMemcpyDeviceToHost, st) != cudaSuccess) return SFA_ERR_CUDA;
+    if (cudaMemcpyAsync(lse_host, lse_dev, lb, cudaMemcpyDeviceToHost, st) != cudaSuccess) return SFA_ERR_CUDA;
+    if (cudaMemcpyAsync(&status, (uint8_t *)scratch + L.status, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        return SFA_ERR_CUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return SFA_ERR_CUDA;
+    return status ? SFA_ERR_INVALID_INPUT : SFA_OK;
+}
+
+int32_t sfa_device_supported(void) {
+    int dev = 0, major = 0, minor = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    return major == 10 && minor == 0;
+}
+
+}  // extern "C"

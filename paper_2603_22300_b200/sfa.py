@@ -1,0 +1,225 @@
+"""Thin Python binding of the C ABI in include/sfa.h (argument marshalling only).
+
+Every step of the hot path runs in the CUDA kernels of ``libsfa.so``; this module only
+allocates outputs with PyTorch, checks dtypes/devices/contiguity, and passes raw pointers
+and the current CUDA stream.  There is no CPU fallback: if the library is missing the
+import of the library fails loudly (build it with ``python -m paper_2603_22300_b200.build``).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsfa.so")
+
+SFA_F32, SFA_BF16 = 0, 1
+KERNEL_AUTO, KERNEL_SIMT, KERNEL_SM100 = 0, 1, 2
+GEN_IID, GEN_LATTICE, GEN_SKEWED = 0, 1, 2
+_STATUS = {0: "ok", 1: "invalid-argument", 2: "invalid-input", 3: "unsupported", 4: "resource-limit",
+           5: "cuda-error"}
+
+
+class SfaError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        super().__init__(f"{where}: {_STATUS.get(code, code)}")
+        self.code = code
+
+
+class AttnDesc(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int32), ("H", ctypes.c_int32), ("H_kv", ctypes.c_int32),
+                ("d", ctypes.c_int32), ("k", ctypes.c_int32), ("d_v", ctypes.c_int32),
+                ("n_q", ctypes.c_int64), ("n_kv", ctypes.c_int64), ("q_pos0", ctypes.c_int64),
+                ("causal", ctypes.c_int32), ("scale", ctypes.c_float), ("dtype", ctypes.c_int32),
+                ("kernel", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2603_22300_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I32, I64, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+        D = ctypes.POINTER(AttnDesc)
+        sig = {
+            "sfa_status_string": ([I32], ctypes.c_char_p),
+            "sfa_topk_codes": ([P, I32, I64, I32, I64, I32, P, P, P, P], I32),
+            "sfa_attn_workspace_bytes": ([D], SZ),
+            "sfa_attn_fwd": ([D, P, P, P, P, P, P, P, P, SZ, P], I32),
+            "sfa_bucket_keys": ([D, P, P, P, SZ, P], I32),
+            "sfa_attn_fwd_bucketed": ([D, P, P, P, P, P, P, SZ, P], I32),
+            "sfa_key_tile": ([D], I32),
+            "sfa_forward_scratch_bytes": ([D], SZ),
+            "sfa_forward": ([D, P, P, P, P, P, P, SZ, P], I32),
+            "sfa_forward_host": ([D, P, P, P, P, P, P, P, P, P, P, P, SZ, P], I32),
+            "sfa_device_supported": ([], I32),
+            "sfa_gen_fill": ([P, I32, I64, I64, ctypes.c_uint64, I32, I32, I64, I32, I32, P], I32),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes, f.restype = args, res
+        _lib = L
+    return _lib
+
+
+EXPORTS = ("sfa_status_string", "sfa_topk_codes", "sfa_attn_workspace_bytes", "sfa_attn_fwd", "sfa_bucket_keys",
+           "sfa_attn_fwd_bucketed", "sfa_key_tile", "sfa_forward_scratch_bytes", "sfa_forward",
+           "sfa_forward_host", "sfa_device_supported", "sfa_gen_fill")
+
+
+def _check(code: int, where: str):
+    if code != 0:
+        raise SfaError(code, where)
+
+
+def _p(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return SFA_BF16
+    if t.dtype == torch.float32:
+        return SFA_F32
+    raise TypeError(f"unsupported dtype {t.dtype} (bf16 or fp32)")
+
+
+def _dev(*ts):
+    for t in ts:
+        if not (t.is_cuda and t.is_contiguous()):
+            raise ValueError("tensors must be contiguous CUDA tensors")
+
+
+def make_desc(*, B, H, H_kv, d, k, d_v, n_q, n_kv, q_pos0=0, causal=True, scale=None, dtype=SFA_BF16,
+              kernel=KERNEL_AUTO) -> AttnDesc:
+    if scale is None:
+        scale = 1.0 / math.sqrt(d)  # P:L99, reading A5
+    return AttnDesc(B, H, H_kv, d, k, d_v, n_q, n_kv, q_pos0, int(bool(causal)), scale, dtype, kernel)
+
+
+def topk_codes(x: torch.Tensor, k: int, status: torch.Tensor | None = None):
+    """Stage 1: x [..., d] -> (idx u8 [..., k], val [..., k])."""
+    _dev(x)
+    d = x.shape[-1]
+    rows = x.numel() // d
+    idx = torch.empty(x.shape[:-1] + (k,), dtype=torch.uint8, device=x.device)
+    val = torch.empty(x.shape[:-1] + (k,), dtype=x.dtype, device=x.device)
+    _check(lib().sfa_topk_codes(_p(x), _dt(x), rows, d, d, k, _p(idx), _p(val), _p(status), _stream()),
+           "sfa_topk_codes")
+    return idx, val
+
+
+def _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, kernel, dtype):
+    B, H, n_q, k = q_idx.shape
+    _, H_kv, n_kv, _ = k_idx.shape
+    return make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k, d_v=v.shape[-1], n_q=n_q, n_kv=n_kv, q_pos0=q_pos0,
+                     causal=causal, scale=scale, dtype=dtype, kernel=kernel)
+
+
+def workspace_bytes(desc: AttnDesc) -> int:
+    return int(lib().sfa_attn_workspace_bytes(ctypes.byref(desc)))
+
+
+def key_tile(desc: AttnDesc) -> int:
+    return int(lib().sfa_key_tile(ctypes.byref(desc)))
+
+
+def attn_fwd(q_idx, q_val, k_idx, k_val, v, *, d, causal=True, scale=None, q_pos0=0, kernel=KERNEL_AUTO,
+             workspace=None, out=None):
+    """Stage 2: (O, LSE) = FlashSFA forward over the codes (bucketing + attention kernels)."""
+    _dev(q_idx, q_val, k_idx, k_val, v)
+    desc = _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, kernel, _dt(v))
+    B, H, n_q, _ = q_idx.shape
+    nb = workspace_bytes(desc)
+    if workspace is None:
+        workspace = torch.empty(max(nb, 16), dtype=torch.uint8, device=v.device)
+    if out is None:
+        o = torch.empty((B, H, n_q, v.shape[-1]), dtype=v.dtype, device=v.device)
+        lse = torch.empty((B, H, n_q), dtype=torch.float32, device=v.device)
+    else:
+        o, lse = out
+    _check(lib().sfa_attn_fwd(ctypes.byref(desc), _p(q_idx), _p(q_val), _p(k_idx), _p(k_val), _p(v), _p(o),
+                              _p(lse), _p(workspace), workspace.numel(), _stream()), "sfa_attn_fwd")
+    return o, lse
+
+
+def bucket_keys(k_idx, k_val, *, d, n_q=1, H=None, d_v=64, causal=True, workspace=None):
+    """Step 3 alone: the key-tile feature buckets (uint8 workspace tensor)."""
+    _dev(k_idx, k_val)
+    B, H_kv, n_kv, k = k_idx.shape
+    desc = make_desc(B=B, H=H or H_kv, H_kv=H_kv, d=d, k=k, d_v=d_v, n_q=n_q, n_kv=n_kv, causal=causal,
+                     dtype=_dt(k_val))
+    nb = workspace_bytes(desc)
+    if workspace is None:
+        workspace = torch.zeros(max(nb, 16), dtype=torch.uint8, device=k_idx.device)
+    _check(lib().sfa_bucket_keys(ctypes.byref(desc), _p(k_idx), _p(k_val), _p(workspace), workspace.numel(),
+                                 _stream()), "sfa_bucket_keys")
+    return workspace, desc
+
+
+def attn_fwd_bucketed(desc: AttnDesc, q_idx, q_val, v, workspace, out=None):
+    _dev(q_idx, q_val, v, workspace)
+    if out is None:
+        o = torch.empty((desc.B, desc.H, desc.n_q, desc.d_v), dtype=v.dtype, device=v.device)
+        lse = torch.empty((desc.B, desc.H, desc.n_q), dtype=torch.float32, device=v.device)
+    else:
+        o, lse = out
+    _check(lib().sfa_attn_fwd_bucketed(ctypes.byref(desc), _p(q_idx), _p(q_val), _p(v), _p(o), _p(lse),
+                                       _p(workspace), workspace.numel(), _stream()), "sfa_attn_fwd_bucketed")
+    return o, lse
+
+
+def scratch_bytes(desc: AttnDesc) -> int:
+    return int(lib().sfa_forward_scratch_bytes(ctypes.byref(desc)))
+
+
+def forward(q, k, v, *, k_code, causal=True, scale=None, q_pos0=0, kernel=KERNEL_AUTO, scratch=None, out=None):
+    """The whole hot path (stage 1 on Q and K, then stage 2): dense q, k, v -> (O, LSE)."""
+    _dev(q, k, v)
+    B, H, n_q, d = q.shape
+    _, H_kv, n_kv, _ = k.shape
+    desc = make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k_code, d_v=v.shape[-1], n_q=n_q, n_kv=n_kv, q_pos0=q_pos0,
+                     causal=causal, scale=scale, dtype=_dt(v), kernel=kernel)
+    if scratch is None:
+        scratch = torch.empty(max(scratch_bytes(desc), 16), dtype=torch.uint8, device=v.device)
+    if out is None:
+        o = torch.empty((B, H, n_q, v.shape[-1]), dtype=v.dtype, device=v.device)
+        lse = torch.empty((B, H, n_q), dtype=torch.float32, device=v.device)
+    else:
+        o, lse = out
+    _check(lib().sfa_forward(ctypes.byref(desc), _p(q), _p(k), _p(v), _p(o), _p(lse), _p(scratch),
+                             scratch.numel(), _stream()), "sfa_forward")
+    return o, lse
+
+
+def forward_host(desc: AttnDesc, q_host, k_host, v_host, o_host, lse_host, dev_bufs, scratch):
+    """End to end from host (pinned) tensors: H2D copies, the hot path, D2H copies, stream sync."""
+    qd, kd, vd, od, ld = dev_bufs
+    _check(lib().sfa_forward_host(ctypes.byref(desc), _p(q_host), _p(k_host), _p(v_host), _p(o_host),
+                                  _p(lse_host), _p(qd), _p(kd), _p(vd), _p(od), _p(ld), _p(scratch),
+                                  scratch.numel(), _stream()), "sfa_forward_host")
+
+
+def gen_fill(t: torch.Tensor, seed: int, tensor_id: int, variant: int = GEN_IID, offset: int = 0, skew_span: int = 3):
+    """Fill a CUDA tensor [..., n, d] with the seeded generator (bit-identical to inputs.py)."""
+    _dev(t)
+    n = t.shape[-2] if t.dim() >= 2 else 1
+    d = t.shape[-1]
+    _check(lib().sfa_gen_fill(_p(t), _dt(t), t.numel(), offset, seed, tensor_id, variant, n, d, skew_span,
+                              _stream()), "sfa_gen_fill")
+    return t
+
+
+def device_supported() -> bool:
+    return bool(lib().sfa_device_supported())

@@ -1,0 +1,92 @@
+"""CPU-only checks of the C ABI: the library builds/loads, exports every symbol include/*.h
+declares, and rejects bad arguments on the host before touching a device."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    names = set()
+    for h in ("sfa.h", "sfa_gen.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        names |= set(re.findall(r"^SFA_API[^(]*?\b(sfa_\w+)\s*\(", src, flags=re.M))
+    return names
+
+
+@pytest.fixture(scope="module")
+def sfa():
+    from paper_2603_22300_b200 import build, sfa
+    build.build()
+    return sfa
+
+
+def test_exports_every_declared_symbol(sfa):
+    decl = declared_symbols()
+    assert len(decl) >= 12
+    L = sfa.lib()
+    for name in decl:
+        assert hasattr(L, name), name
+    assert set(sfa.EXPORTS) == decl
+
+
+def test_status_strings(sfa):
+    s = sfa.lib().sfa_status_string
+    assert [s(i).decode() for i in range(6)] == ["ok", "invalid-argument", "invalid-input", "unsupported",
+                                                 "resource-limit", "cuda-error"]
+
+
+def test_host_validation_before_launch(sfa):
+    L = sfa.lib()
+    P = ctypes.c_void_p
+    dummy = P(16)
+    # k out of range -> invalid-argument; d not compiled -> unsupported
+    assert L.sfa_topk_codes(dummy, 1, 10, 128, 128, 0, dummy, dummy, None, None) == 1
+    assert L.sfa_topk_codes(dummy, 1, 10, 128, 128, 129, dummy, dummy, None, None) == 1
+    assert L.sfa_topk_codes(dummy, 1, 10, 96, 96, 8, dummy, dummy, None, None) == 3
+    assert L.sfa_topk_codes(dummy, 7, 10, 128, 128, 8, dummy, dummy, None, None) == 1
+    assert L.sfa_topk_codes(None, 1, 10, 128, 128, 8, dummy, dummy, None, None) == 1
+    assert L.sfa_topk_codes(dummy, 1, 0, 128, 128, 8, None, None, None, None) == 0  # empty is ok
+
+
+def desc(sfa, **kw):
+    base = dict(B=1, H=4, H_kv=2, d=128, k=16, d_v=128, n_q=300, n_kv=300)
+    base.update(kw)
+    return sfa.make_desc(**base)
+
+
+def test_desc_validation(sfa):
+    L = sfa.lib()
+    ok = desc(sfa)
+    assert L.sfa_attn_workspace_bytes(ctypes.byref(ok)) > 0
+    bad = [dict(H=3, H_kv=2), dict(k=0), dict(k=129), dict(n_q=0), dict(n_kv=0), dict(scale=-1.0),
+           dict(scale=float("inf")), dict(q_pos0=-1)]
+    for b in bad:
+        d = desc(sfa, **b)
+        assert L.sfa_attn_workspace_bytes(ctypes.byref(d)) == 0, b
+        assert L.sfa_attn_fwd(ctypes.byref(d), *([ctypes.c_void_p(16)] * 8), 1 << 30, None) == 1, b
+    for b in (dict(d=96, k=8), dict(d_v=96), dict(dtype=sfa.SFA_F32, kernel=sfa.KERNEL_SM100)):
+        d = desc(sfa, **b)
+        assert L.sfa_attn_fwd(ctypes.byref(d), *([ctypes.c_void_p(16)] * 8), 1 << 30, None) == 3, b
+    # workspace too small -> resource-limit
+    assert L.sfa_attn_fwd(ctypes.byref(ok), *([ctypes.c_void_p(16)] * 8), 16, None) == 4
+    # misaligned pointers -> invalid-argument
+    assert L.sfa_attn_fwd(ctypes.byref(ok), *([ctypes.c_void_p(18)] * 8), 1 << 30, None) == 1
+
+
+def test_workspace_layout(sfa):
+    """Key-tile bucket layout: per (b, kv head, tile) off[d+1] u16 (16-aligned) +
+    (BK*k + 3d rounded to 4) entries of 4 B (bf16) or 8 B (fp32)."""
+    L = sfa.lib()
+    for (k, bk) in ((8, 128), (16, 128), (32, 128), (64, 64), (128, 64)):
+        for dt, eb in ((sfa.SFA_BF16, 4), (sfa.SFA_F32, 8)):
+            d = desc(sfa, k=k, dtype=dt)
+            assert L.sfa_key_tile(ctypes.byref(d)) == bk
+            off = (129 * 2 + 15) // 16 * 16
+            cap = (bk * k + 3 * 128 + 3) // 4 * 4
+            tile = (off + cap * eb + 15) // 16 * 16
+            ntiles = (300 + bk - 1) // bk
+            assert L.sfa_attn_workspace_bytes(ctypes.byref(d)) == 1 * 2 * ntiles * tile

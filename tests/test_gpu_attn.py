@@ -1,0 +1,233 @@
+"""GPU parity of stage 2 (sfa_attn_fwd) and of the whole path (sfa_forward) against the oracle.
+
+Inputs are seeded and synthetic.  The oracle always recomputes the
+codes itself from the host-regenerated dense inputs: no oracle input comes from the CUDA path.
+Small configs are compared element by element; the BASELINE-size configs (Qwen3-32K, sweep,
+long) on sampled rows (first/last rows, tile boundaries +-1, random rows in every head).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from helpers import assert_attn_close, from_torch, host_qkv, oracle_codes, to_torch
+from paper_2603_22300_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+KERNELS = {"simt": 1, "auto": 0}
+
+
+def gpu_attn(lib, qi, qv, ki, kv, v, dtype, d, **kw):
+    import torch
+    o, lse = lib.attn_fwd(to_torch(qi, "u8"), to_torch(qv, dtype), to_torch(ki, "u8"), to_torch(kv, dtype),
+                          to_torch(v, dtype), d=d, **kw)
+    torch.cuda.synchronize()
+    return from_torch(o), from_torch(lse)
+
+
+def run_case(lib, seed, B, H, H_kv, n, d, d_v, k, dtype, causal=True, variant="iid", kernel=0, n_kv=None,
+             q_pos0=0):
+    q, kx, v = host_qkv(seed, B, H, H_kv, n, d, d_v, dtype, variant=variant, n_kv=n_kv)
+    qi, qv = oracle_codes(q, k)
+    ki, kv = oracle_codes(kx, k)
+    o_ref, l_ref = oracle.attn_fwd(qi, qv, ki, kv, v, d=d, causal=causal, q_pos0=q_pos0)
+    o, lse = gpu_attn(lib, qi, qv, ki, kv, v, dtype, d, causal=causal, kernel=kernel, q_pos0=q_pos0)
+    return assert_attn_close(o, lse, o_ref, l_ref, dtype)
+
+
+@pytest.mark.parametrize("kernel", list(KERNELS))
+def test_tiny_config(lib, kernel):
+    """BASELINE configs[0]: B=1,H=1,n=256,d=64,k=8, causal, fp32 -> 1e-5 relative."""
+    for seed in (1, 2, 3):
+        run_case(lib, seed, 1, 1, 1, 256, 64, 64, 8, "f32", kernel=KERNELS[kernel])
+    run_case(lib, 2, 1, 1, 1, 256, 64, 64, 8, "f32", variant="lattice", kernel=KERNELS[kernel])
+
+
+@pytest.mark.parametrize("kernel", list(KERNELS))
+def test_gpt2_config(lib, kernel):
+    """BASELINE configs[1]: B=8,H=12,n=1024,d=64,k=8, causal, bf16 V -> 2e-3 max-abs, every element."""
+    run_case(lib, 11, 8, 12, 12, 1024, 64, 64, 8, "bf16", kernel=KERNELS[kernel])
+
+
+@pytest.mark.parametrize("kernel", list(KERNELS))
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("causal", [True, False])
+@pytest.mark.parametrize("shape", [
+    (1, 4, 2, 300, 128, 128, 16),    # GQA, ragged n (not a multiple of 128)
+    (2, 2, 1, 129, 64, 128, 8),      # tile boundary + 1
+    (1, 1, 1, 1, 128, 64, 4),        # single token
+    (1, 2, 2, 200, 128, 128, 128),   # k = d (BK = 64)
+    (1, 2, 1, 190, 128, 64, 64),     # k = 64 (BK = 64), ragged
+    (1, 1, 1, 77, 64, 64, 1),        # k = 1
+])
+def test_shapes(lib, kernel, dtype, causal, shape):
+    if dtype == "f32" and kernel == "sm100":
+        pytest.skip("sm100 kernel is bf16 only")
+    B, H, H_kv, n, d, d_v, k = shape
+    run_case(lib, 7, B, H, H_kv, n, d, d_v, k, dtype, causal=causal, kernel=KERNELS[kernel])
+
+
+@pytest.mark.parametrize("kernel", list(KERNELS))
+def test_skewed_and_lattice(lib, kernel):
+    run_case(lib, 5, 1, 4, 2, 384, 128, 128, 16, "bf16", variant="skewed", kernel=KERNELS[kernel])
+    run_case(lib, 6, 1, 2, 2, 256, 128, 128, 16, "bf16", variant="lattice", kernel=KERNELS[kernel])
+
+
+@pytest.mark.parametrize("kernel", list(KERNELS))
+def test_q_pos0_chunks_equal_full(lib, kernel):
+    """A query chunk at global offset q_pos0 (the sharded path, reading A9) reproduces the
+    full run's rows bit-for-bit; also checked against the oracle."""
+    B, H, H_kv, n, d, d_v, k = 1, 4, 2, 640, 128, 128, 16
+    q, kx, v = host_qkv(9, B, H, H_kv, n, d, d_v, "bf16")
+    qi, qv = oracle_codes(q, k)
+    ki, kv = oracle_codes(kx, k)
+    o, lse = gpu_attn(lib, qi, qv, ki, kv, v, "bf16", d, kernel=KERNELS[kernel])
+    for a, b in ((0, 128), (128, 384), (384, 640), (200, 333)):
+        oc, lc = gpu_attn(lib, qi[:, :, a:b], qv[:, :, a:b], ki, kv, v, "bf16", d, kernel=KERNELS[kernel], q_pos0=a)
+        np.testing.assert_array_equal(oc, o[:, :, a:b])
+        np.testing.assert_array_equal(lc, lse[:, :, a:b])
+    o_ref, l_ref = oracle.attn_fwd(qi[:, :, 200:333], qv[:, :, 200:333], ki, kv, v, d=d, q_pos0=200)
+    oc, lc = gpu_attn(lib, qi[:, :, 200:333], qv[:, :, 200:333], ki, kv, v, "bf16", d, kernel=KERNELS[kernel],
+                      q_pos0=200)
+    assert_attn_close(oc, lc, o_ref, l_ref, "bf16")
+
+
+@pytest.mark.parametrize("kernel", list(KERNELS))
+def test_disjoint_supports_prefix_mean(lib, kernel):
+    """Disjoint supports: every logit is 0 (A1) -> O_i = mean(V[0..i]), LSE_i = ln(i+1)."""
+    n, d, k, d_v = 300, 128, 16, 128
+    qi = np.tile(np.arange(k, dtype=np.uint8), (1, 1, n, 1))
+    ki = np.tile(np.arange(64, 64 + k, dtype=np.uint8), (1, 1, n, 1))
+    qv = inputs.gen(1, 1, (1, 1, n, k), "bf16")
+    kv = inputs.gen(1, 2, (1, 1, n, k), "bf16")
+    v = inputs.gen(1, 3, (1, 1, n, d_v), "bf16")
+    o, lse = gpu_attn(lib, qi, qv, ki, kv, v, "bf16", d, kernel=KERNELS[kernel])
+    vf = inputs.bf16_bits_to_f32(v)[0, 0].astype(np.float64)
+    cm = np.cumsum(vf, 0) / np.arange(1, n + 1)[:, None]
+    assert_attn_close(o[0, 0], lse[0, 0], cm, np.log(np.arange(1, n + 1)), "bf16")
+
+
+@pytest.mark.parametrize("kernel", list(KERNELS))
+def test_determinism_and_causality(lib, kernel):
+    B, H, H_kv, n, d, d_v, k = 1, 2, 1, 400, 128, 128, 16
+    q, kx, v = host_qkv(10, B, H, H_kv, n, d, d_v, "bf16")
+    qi, qv = oracle_codes(q, k)
+    ki, kv = oracle_codes(kx, k)
+    o1, l1 = gpu_attn(lib, qi, qv, ki, kv, v, "bf16", d, kernel=KERNELS[kernel])
+    o2, l2 = gpu_attn(lib, qi, qv, ki, kv, v, "bf16", d, kernel=KERNELS[kernel])
+    assert np.array_equal(o1, o2) and np.array_equal(l1, l2)
+    i = 150
+    kv2, v2 = kv.copy(), v.copy()
+    kv2[:, :, i + 1:] = inputs.gen(77, 2, kv2[:, :, i + 1:].shape, "bf16")
+    v2[:, :, i + 1:] = inputs.gen(78, 3, v2[:, :, i + 1:].shape, "bf16")
+    o3, l3 = gpu_attn(lib, qi, qv, ki, kv2, v2, "bf16", d, kernel=KERNELS[kernel])
+    assert np.array_equal(o3[:, :, :i + 1], o1[:, :, :i + 1]) and np.array_equal(l3[:, :, :i + 1], l1[:, :, :i + 1])
+
+
+def test_k_equals_d_dense(lib):
+    """k = d: the path must equal dense softmax attention (north star); oracle pinned to torch SDPA."""
+    run_case(lib, 41, 1, 4, 2, 512, 128, 128, 128, "bf16")
+
+
+def test_forward_composition_and_host(lib):
+    """sfa_forward (stage 1 on Q and K + stage 2) equals the two stages called separately,
+    and sfa_forward_host (host buffers, copies inside) equals sfa_forward bitwise."""
+    import torch
+    B, H, H_kv, n, d, d_v, k = 1, 4, 2, 513, 128, 128, 16
+    q, kx, v = host_qkv(12, B, H, H_kv, n, d, d_v, "bf16")
+    Q, K, V = to_torch(q, "bf16"), to_torch(kx, "bf16"), to_torch(v, "bf16")
+    o, lse = lib.forward(Q, K, V, k_code=k)
+    qi, qv = lib.topk_codes(Q, k)
+    ki, kv = lib.topk_codes(K, k)
+    o2, l2 = lib.attn_fwd(qi, qv, ki, kv, V, d=d)
+    torch.cuda.synchronize()
+    assert torch.equal(o, o2) and torch.equal(lse, l2)
+    desc = lib.make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k, d_v=d_v, n_q=n, n_kv=n)
+    scratch = torch.empty(lib.scratch_bytes(desc), dtype=torch.uint8, device="cuda")
+    pin = lambda t: t.cpu().pin_memory()
+    qh, kh, vh = pin(Q), pin(K), pin(V)
+    oh = torch.empty(o.shape, dtype=o.dtype).pin_memory()
+    lh = torch.empty(lse.shape, dtype=torch.float32).pin_memory()
+    bufs = (torch.empty_like(Q), torch.empty_like(K), torch.empty_like(V), torch.empty_like(o), torch.empty_like(lse))
+    lib.forward_host(desc, qh, kh, vh, oh, lh, bufs, scratch)
+    assert torch.equal(oh, o.cpu()) and torch.equal(lh, lse.cpu())
+    o_ref, l_ref = oracle.attn_fwd(*oracle_codes(q, k), *oracle_codes(kx, k), v, d=d)
+    assert_attn_close(from_torch(o), from_torch(lse), o_ref, l_ref, "bf16")
+
+
+def test_forward_host_nonfinite(lib):
+    import torch
+    B, H, H_kv, n, d, d_v, k = 1, 1, 1, 64, 64, 64, 8
+    q, kx, v = host_qkv(1, B, H, H_kv, n, d, d_v, "f32")
+    q[0, 0, 5, 7] = np.nan
+    desc = lib.make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k, d_v=d_v, n_q=n, n_kv=n, dtype=lib.SFA_F32)
+    scratch = torch.empty(lib.scratch_bytes(desc), dtype=torch.uint8, device="cuda")
+    Q, K, V = (torch.from_numpy(a).pin_memory() for a in (q, kx, v))
+    oh = torch.empty((B, H, n, d_v)).pin_memory()
+    lh = torch.empty((B, H, n)).pin_memory()
+    bufs = tuple(torch.empty(t.shape, device="cuda") for t in (Q, K, V, oh, lh))
+    with pytest.raises(lib.SfaError) as e:
+        lib.forward_host(desc, Q, K, V, oh, lh, bufs, scratch)
+    assert e.value.code == 2
+
+
+# ---------------------------------------------------------------------------------------------
+# BASELINE-size configs on sampled rows (device-generated inputs, host-regenerated oracle inputs)
+# ---------------------------------------------------------------------------------------------
+def sampled_rows(B, H, n, bq=128, per_head=16, seed=0):
+    rng = np.random.default_rng(seed)
+    rows = []
+    for bh in range(B * H):
+        cand = {0, 1, n - 1, n - 2}
+        for t in (bq, 2 * bq, n // 2, n - bq):
+            cand |= {t - 1, t, t + 1}
+        cand |= set(rng.integers(0, n, per_head).tolist())
+        rows += [bh * n + i for i in sorted(c for c in cand if 0 <= c < n)]
+    return np.array(rows, np.int64)
+
+
+def big_case(lib, seed, B, H, H_kv, n, d, d_v, k, kernel=0, per_head=16):
+    import torch
+    dev = "cuda"
+    Q = lib.gen_fill(torch.empty((B, H, n, d), dtype=torch.bfloat16, device=dev), seed, inputs.TID_Q)
+    K = lib.gen_fill(torch.empty((B, H_kv, n, d), dtype=torch.bfloat16, device=dev), seed, inputs.TID_K)
+    V = lib.gen_fill(torch.empty((B, H_kv, n, d_v), dtype=torch.bfloat16, device=dev), seed, inputs.TID_V)
+    o, lse = lib.forward(Q, K, V, k_code=k, kernel=kernel)
+    torch.cuda.synchronize()
+    del Q
+    rows = sampled_rows(B, H, n, per_head=per_head, seed=seed)
+    # oracle inputs regenerated on the host: the sampled query rows, all keys and values
+    qflat = (rows[:, None] * d + np.arange(d)[None, :])
+    q_rows = inputs.gen(seed, inputs.TID_Q, (B, H, n, d), "bf16", flat=qflat)
+    kx = inputs.gen(seed, inputs.TID_K, (B, H_kv, n, d), "bf16")
+    v = inputs.gen(seed, inputs.TID_V, (B, H_kv, n, d_v), "bf16")
+    ki, kv = oracle_codes(kx, k)
+    qi_r, qv_r = oracle_codes(q_rows, k)
+    # scatter the sampled query codes into a full-size code tensor (other rows unused by the oracle)
+    qi = np.zeros((B, H, n, k), np.uint8)
+    qv = np.zeros((B, H, n, k), np.uint16)
+    qi.reshape(-1, k)[rows] = qi_r
+    qv.reshape(-1, k)[rows] = qv_r
+    o_ref, l_ref = oracle.attn_fwd(qi, qv, ki, kv, v, d=d, rows=rows)
+    og = from_torch(o).reshape(-1, d_v)[rows]
+    lg = from_torch(lse).reshape(-1)[rows]
+    return assert_attn_close(og, lg, o_ref, l_ref, "bf16")
+
+
+@pytest.mark.slow
+def test_qwen3_config_sampled(lib):
+    """BASELINE configs[2]: B=1, H=32 (8 KV heads), n=32768, d=128, k=16, causal, bf16."""
+    big_case(lib, 21, 1, 32, 8, 32768, 128, 128, 16)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("k", [4, 8, 16, 32, 64, 128])
+def test_sweep_config_sampled(lib, k):
+    """BASELINE configs[4]: k in {4..128=d} at n=16K, d=128 (Qwen3 heads)."""
+    big_case(lib, 41, 1, 32, 8, 16384, 128, 128, k, per_head=4)
+
+
+@pytest.mark.slow
+def test_long_config_sampled(lib):
+    """BASELINE configs[3] at n=131072 on one GPU (the sharded runs must reproduce it)."""
+    big_case(lib, 31, 1, 32, 8, 131072, 128, 128, 16, per_head=2)
