@@ -234,16 +234,16 @@ def main():
     dcode = desc.dtype
 
     def step(ev=None):
-        # stage 1 on Q, stage 1 on K, step 3 bucketing, steps 4-8 attention -- 4 launches of ours
+        # stage 1 on Q, stage 1 on K, step 3 (V prep for sm100 / buckets for simt), steps 4-8 attention
         if ev: ev[0].record()
         r1 = L.sfa_topk_codes(P(Q), dcode, B * H * n, d, d, k, P(q_idx), P(q_val), P(status), st())
         if ev: ev[1].record()
         r2 = L.sfa_topk_codes(P(K), dcode, B * H_kv * n, d, d, k, P(k_idx), P(k_val), P(status), st())
         if ev: ev[2].record()
-        r3 = L.sfa_bucket_keys(ctypes.byref(desc), P(k_idx), P(k_val), P(ws), ws.numel(), st())
+        r3 = L.sfa_attn_prepare(ctypes.byref(desc), P(k_idx), P(k_val), P(V), P(ws), ws.numel(), st())
         if ev: ev[3].record()
-        r4 = L.sfa_attn_fwd_bucketed(ctypes.byref(desc), P(q_idx), P(q_val), P(V), P(O), P(LSE), P(ws), ws.numel(),
-                                     st())
+        r4 = L.sfa_attn_fwd_prepared(ctypes.byref(desc), P(q_idx), P(q_val), P(k_idx), P(k_val), P(V), P(O), P(LSE),
+                                     P(ws), ws.numel(), st())
         if ev: ev[4].record()
         if r1 or r2 or r3 or r4:
             raise RuntimeError(f"sfa call failed: {(r1, r2, r3, r4)}")
@@ -326,11 +326,16 @@ def main():
         except Exception:
             traffic = None
     topk_bytes = W.topk_bytes()
-    roofline = {"bound": "alu", "kernel": "sfa attention (steps 4-8)", "achieved": achieved / 1e9,
-                "peak": mufu_peak / 1e9, "unit": "G pairs/s (1 MUFU ex2 per allowed pair)",
+    sm100 = W.dtype == "bf16" and args.kernel != "simt"
+    roofline = {"bound": "alu", "kernel": ("attn_sm100_kernel" if sm100 else "attn_simt_kernel") + " (steps 4-8)",
+                "achieved": achieved / 1e9, "peak": mufu_peak / 1e9,
+                "unit": "G pairs/s (1 MUFU ex2 per allowed causal pair)",
                 "frac": achieved / mufu_peak, "traffic": traffic,
-                "peak_source": f"148 SMs x 16 ex2/clk x {pk['sm_max_mhz']:.0f} MHz (DESIGN.md)",
+                "peak_source": f"148 SMs x 16 ex2/clk x {pk['sm_max_mhz']:.0f} MHz (DESIGN.md 'Rooflines')",
                 "other_floors": {
+                    # tensor pipe: S = Q~K~^T (2d) + P.V (2 d_v) FLOPs per allowed pair, vs the measured bf16 peak
+                    "tensor_frac": (2.0 * (d + d_v) * pairs / (attn_ms / 1e3)) / (pk["bf16_tflops"] * 1e12)
+                    if sm100 else None,
                     "tensor_pv_frac": (2.0 * d_v * pairs / (attn_ms / 1e3)) / (pk["bf16_tflops"] * 1e12),
                     "hbm_attn_frac": (W.attn_min_bytes() / (attn_ms / 1e3)) / (pk["hbm_gbs"] * 1e9),
                     "topk_hbm_gbs": topk_bytes / ((stage_ms[0] + stage_ms[1]) / 1e3) / 1e9,
@@ -348,12 +353,12 @@ def main():
                 "vs_baseline": None, "dtype": W.dtype,
                 "data": "synthetic (seeded counter-based generator on device, DESIGN.md input recipe)",
                 "config": config_of(args, W),
-                "stage_ms": {"topk_q": stage_ms[0], "topk_k": stage_ms[1], "bucket": stage_ms[2],
+                "stage_ms": {"topk_q": stage_ms[0], "topk_k": stage_ms[1], "prepare": stage_ms[2],
                              "attn": stage_ms[3]},
                 "interactions_per_s": W.expected_interactions / (ms_per_step / 1e3) * world,
                 "pairs_per_s": pairs * world / (ms_per_step / 1e3),
                 "wall_s_timed_region": t_wall,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": 4 * args.steps,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (5 if sm100 else 4) * args.steps,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -55,9 +55,11 @@ typedef enum { SFA_F32 = 0, SFA_BF16 = 1 } sfa_dtype;
 
 /* Kernel selection for sfa_attn_fwd (desc.kernel). */
 typedef enum {
-    SFA_KERNEL_AUTO = 0, /* the fastest kernel compiled for the shape                               */
-    SFA_KERNEL_SIMT = 1, /* CUDA-core kernel: bucket scatter + FFMA P.V (the only fp32 P.V path: A12) */
-    SFA_KERNEL_SM100 = 2 /* sm_100a kernel: bucket scatter + tcgen05 P.V, O and P in TMEM (bf16 only) */
+    SFA_KERNEL_AUTO = 0, /* SM100 for bf16, SIMT for fp32                                              */
+    SFA_KERNEL_SIMT = 1, /* CUDA-core kernel: key-tile feature buckets, shared-memory scatter of the
+                            support overlaps, FFMA P.V (the only fp32 path: reading A12)             */
+    SFA_KERNEL_SM100 = 2 /* sm_100a kernel (bf16 only): key codes decompressed on chip, S = Q~ K~^T and
+                            O += P V on tcgen05 tensor cores, S/P/O in TMEM, V by TMA    */
 } sfa_kernel;
 
 SFA_API const char *sfa_status_string(sfa_status s);
@@ -90,28 +92,45 @@ typedef struct {
     int32_t kernel;      /* sfa_kernel; SFA_KERNEL_AUTO unless benchmarking an ablation                   */
 } sfa_attn_desc;
 
-/* Bytes of device workspace sfa_attn_fwd needs: the key-tile feature buckets (DESIGN.md
- * "Key-tile bucketing", our form of the paper's CSC_feat). 0 on invalid desc. */
+/* Bytes of device workspace sfa_attn_fwd needs (0 on an invalid desc):
+ *   SIMT kernel : the key-tile feature buckets (our form of the
+ *                 paper's CSC_feat);
+ *   SM100 kernel: max|V| per (b, kv head) + an fp16 copy of V scaled by a power of two per
+ *                 (b, kv head) -- the exact fp16 P.V operand (reading A12). */
 SFA_API size_t sfa_attn_workspace_bytes(const sfa_attn_desc *desc);
 
 /* O, LSE = FlashSFA forward.
  *   q_idx [B][H][n_q][k] u8,  q_val [B][H][n_q][k]   (stage-1 codes of Q)
  *   k_idx [B][H_kv][n_kv][k] u8, k_val [B][H_kv][n_kv][k]
  *   v     [B][H_kv][n_kv][d_v]       o [B][H][n_q][d_v] (dtype)       lse [B][H][n_q] fp32, natural log
- *   workspace: >= sfa_attn_workspace_bytes(desc) device bytes (else SFA_ERR_RESOURCE).
- *   Launches the bucketing kernel and the attention kernel on `stream`.
+ *   workspace: >= sfa_attn_workspace_bytes(desc) device bytes (else SFA_ERR_RESOURCE), 16-aligned.
+ *   Code and value pointers must be 16-byte aligned.
+ *   Launches (SIMT) the bucketing kernel + the attention kernel, or (SM100) the two V-prep kernels
+ *   + the attention kernel, on `stream`.
  *   O is rounded to the output dtype with round-to-nearest-even (A21). Rows with no allowed key
  *   (impossible when q_pos0 >= 0) get O = 0, LSE = -inf (A10). */
 SFA_API sfa_status sfa_attn_fwd(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val, const uint8_t *k_idx,
                         const void *k_val, const void *v, void *o, float *lse, void *workspace,
                         size_t workspace_bytes, sfa_stream_t stream);
 
-/* Step 3 alone (exposed for tests and for the sharded path, which buckets the gathered keys once):
+/* sfa_attn_fwd in two calls (the sharded path prepares the gathered keys once; the bench times
+ * the attention kernel alone):
+ *   sfa_attn_prepare      -- step 3 for the kernel desc selects: key-tile buckets (SIMT) or max|V|
+ *                            and the scaled fp16 V (SM100), written into `workspace`;
+ *   sfa_attn_fwd_prepared -- steps 4-8 over that workspace (same desc, codes and V). */
+SFA_API sfa_status sfa_attn_prepare(const sfa_attn_desc *desc, const uint8_t *k_idx, const void *k_val, const void *v,
+                                    void *workspace, size_t workspace_bytes, sfa_stream_t stream);
+SFA_API sfa_status sfa_attn_fwd_prepared(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val,
+                                         const uint8_t *k_idx, const void *k_val, const void *v, void *o, float *lse,
+                                         const void *workspace, size_t workspace_bytes, sfa_stream_t stream);
+
+/* SIMT only -- step 3 alone (exposed for the bucket-layout tests):
  * builds the buckets of every key tile into `workspace` (layout in DESIGN.md).  sfa_attn_fwd calls it. */
 SFA_API sfa_status sfa_bucket_keys(const sfa_attn_desc *desc, const uint8_t *k_idx, const void *k_val, void *workspace,
                            size_t workspace_bytes, sfa_stream_t stream);
 
-/* Attention over buckets already built by sfa_bucket_keys (same desc, same workspace). */
+/* SIMT only -- attention over buckets already built by sfa_bucket_keys (same desc, same workspace).
+ * Both return SFA_ERR_UNSUPPORTED for a desc that selects the SM100 kernel. */
 SFA_API sfa_status sfa_attn_fwd_bucketed(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val,
                                  const void *v, void *o, float *lse, const void *workspace,
                                  size_t workspace_bytes, sfa_stream_t stream);
@@ -136,6 +155,16 @@ SFA_API sfa_status sfa_forward(const sfa_attn_desc *desc, const void *q, const v
 SFA_API sfa_status sfa_forward_host(const sfa_attn_desc *desc, const void *q_host, const void *k_host, const void *v_host,
                             void *o_host, float *lse_host, void *q_dev, void *k_dev, void *v_dev, void *o_dev,
                             float *lse_dev, void *scratch, size_t scratch_bytes, sfa_stream_t stream);
+
+/* Diagnostic (tests only): runs sfa_attn_fwd with the sm_100a kernel (desc->dtype must be bf16 and
+ * desc->kernel not SIMT) and also writes the raw fp32 score tile S = Q~ K~^T (unscaled sums of
+ * support overlaps) of the first key tile of work item 0 -- query tile 0, the last
+ * query block of head 0 (batch 0) -- to `scores` [128][128] (device).  Lets a test check the
+ * tensor-core score contraction apart from the softmax and P.V. */
+SFA_API sfa_status sfa_debug_sm100_scores(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val,
+                                          const uint8_t *k_idx, const void *k_val, const void *v, void *o,
+                                          float *lse, void *workspace, size_t workspace_bytes, float *scores,
+                                          sfa_stream_t stream);
 
 /* Build / device info: 1 if the calling thread's current device is sm_100 and the kernels load. */
 SFA_API int32_t sfa_device_supported(void);

@@ -38,10 +38,22 @@ BucketLayout layout_of(const sfa_attn_desc *d) {
     return make_layout(d->d, d->k, d->n_kv, key_tile(d->k), d->dtype == SFA_BF16);
 }
 
-size_t ws_bytes(const sfa_attn_desc *d) {
+// Which attention kernel a desc runs: the sm_100a tensor-core kernel for bf16 unless the caller
+// asks for the CUDA-core kernel, which is also the only fp32 kernel (reading A12).
+bool uses_simt(const sfa_attn_desc *d) { return d->kernel == SFA_KERNEL_SIMT || d->dtype == SFA_F32; }
+
+size_t bucket_bytes(const sfa_attn_desc *d) {
     const BucketLayout L = layout_of(d);
     return (size_t)d->B * d->H_kv * L.ntiles * L.tile_bytes;
 }
+
+// sm100 workspace: [max|V| per (b, kv head), 256-aligned][fp16 copy of V scaled by 2^-e] (vprep.cu);
+// the sm100 kernel decompresses key codes on chip and needs no buckets
+size_t vprep_amax_bytes(const sfa_attn_desc *d) { return align_up((int64_t)d->B * d->H_kv * 4, 256); }
+size_t vprep_bytes(const sfa_attn_desc *d) {
+    return vprep_amax_bytes(d) + (size_t)d->B * d->H_kv * d->n_kv * d->d_v * 2;
+}
+size_t ws_bytes(const sfa_attn_desc *d) { return uses_simt(d) ? bucket_bytes(d) : vprep_bytes(d); }
 
 size_t esize(sfa_dtype t) { return t == SFA_BF16 ? 2 : 4; }
 
@@ -63,23 +75,54 @@ Scratch scratch_layout(const sfa_attn_desc *d) {
     return s;
 }
 
-sfa_status run_attn(const sfa_attn_desc *d, const uint8_t *q_idx, const void *q_val, const void *v, void *o,
-                    float *lse, const void *ws, cudaStream_t st) {
+AttnParams make_params(const sfa_attn_desc *d, const uint8_t *q_idx, const void *q_val, const uint8_t *k_idx,
+                       const void *k_val, const void *v, void *o, float *lse, const void *ws) {
     AttnParams p;
-    p.q_idx = q_idx; p.q_val = q_val; p.v = v; p.o = o; p.lse = lse; p.ws = (const uint8_t *)ws;
+    p.q_idx = q_idx; p.q_val = q_val; p.k_idx = k_idx; p.k_val = k_val;
+    p.v = v; p.o = o; p.lse = lse; p.ws = (const uint8_t *)ws;
+    p.v_amax = (const uint32_t *)ws;
+    p.v16 = ws ? (const uint8_t *)ws + vprep_amax_bytes(d) : nullptr;
     p.B = d->B; p.H = d->H; p.H_kv = d->H_kv; p.k = d->k;
     p.n_q = d->n_q; p.n_kv = d->n_kv; p.q_pos0 = d->q_pos0; p.causal = d->causal;
     p.scale_log2 = d->scale * kLog2e;
     p.L = layout_of(d);
-    const bool bf16 = d->dtype == SFA_BF16;
-    if (bf16 && d->kernel != SFA_KERNEL_SIMT) {
-        cudaError_t e = launch_attn_sm100(p, d->d, d->d_v, st);
-        if (e == cudaSuccess) return SFA_OK;
-        if (e != cudaErrorNotSupported || d->kernel == SFA_KERNEL_SM100) return e == cudaErrorNotSupported ? SFA_ERR_UNSUPPORTED : SFA_ERR_CUDA;
-        (void)cudaGetLastError();
-    }
-    return from_cuda(launch_attn_simt(p, bf16, d->d, d->d_v, st));
+    return p;
 }
+
+sfa_status from_launch(cudaError_t e) {
+    if (e == cudaSuccess) return SFA_OK;
+    (void)cudaGetLastError();
+    return e == cudaErrorNotSupported ? SFA_ERR_UNSUPPORTED : SFA_ERR_CUDA;
+}
+
+// step 3: what the chosen attention kernel reads besides the codes -- key-tile buckets (SIMT) or
+// max|V| + the scaled fp16 V (SM100)
+sfa_status run_prepare(const sfa_attn_desc *d, const uint8_t *k_idx, const void *k_val, const void *v, void *ws,
+                       cudaStream_t st) {
+    const AttnParams p = make_params(d, nullptr, nullptr, k_idx, k_val, v, nullptr, nullptr, ws);
+    if (uses_simt(d))
+        return from_cuda(launch_bucket(k_idx, k_val, d->dtype == SFA_BF16, d->d, d->k, (int64_t)d->B * d->H_kv,
+                                       d->n_kv, p.L, ws, st));
+    return from_cuda(launch_vprep(v, (int64_t)d->B * d->H_kv, d->n_kv, d->d_v, (uint32_t *)p.v_amax, (void *)p.v16, st));
+}
+
+// steps 4-8 over a prepared workspace
+sfa_status run_attn_prepared(const sfa_attn_desc *d, const uint8_t *q_idx, const void *q_val, const uint8_t *k_idx,
+                             const void *k_val, const void *v, void *o, float *lse, void *ws, cudaStream_t st,
+                             float *dbg = nullptr) {
+    const AttnParams p = make_params(d, q_idx, q_val, k_idx, k_val, v, o, lse, ws);
+    if (!uses_simt(d)) return from_launch(launch_attn_sm100(p, d->d, d->d_v, st, dbg));
+    return from_cuda(launch_attn_simt(p, d->dtype == SFA_BF16, d->d, d->d_v, st));
+}
+
+sfa_status run_attn(const sfa_attn_desc *d, const uint8_t *q_idx, const void *q_val, const uint8_t *k_idx,
+                    const void *k_val, const void *v, void *o, float *lse, void *ws, cudaStream_t st) {
+    sfa_status s = run_prepare(d, k_idx, k_val, v, ws, st);
+    if (s != SFA_OK) return s;
+    return run_attn_prepared(d, q_idx, q_val, k_idx, k_val, v, o, lse, ws, st);
+}
+
+bool codes_aligned(const void *a, const void *b) { return aligned16(a) && aligned16(b); }
 
 }  // namespace
 
@@ -125,6 +168,7 @@ sfa_status sfa_bucket_keys(const sfa_attn_desc *desc, const uint8_t *k_idx, cons
                            size_t workspace_bytes, sfa_stream_t stream) {
     sfa_status s = validate_desc(desc);
     if (s != SFA_OK) return s;
+    if (!uses_simt(desc)) return SFA_ERR_UNSUPPORTED;  // buckets feed the CUDA-core kernel only
     if (!k_idx || !k_val || !workspace || !aligned16(workspace)) return SFA_ERR_INVALID_ARGUMENT;
     if (workspace_bytes < ws_bytes(desc)) return SFA_ERR_RESOURCE;
     return from_cuda(launch_bucket(k_idx, k_val, desc->dtype == SFA_BF16, desc->d, desc->k,
@@ -140,8 +184,10 @@ sfa_status sfa_attn_fwd_bucketed(const sfa_attn_desc *desc, const uint8_t *q_idx
     if (!q_idx || !q_val || !v || !o || !lse || !workspace) return SFA_ERR_INVALID_ARGUMENT;
     if (!aligned16(v) || !aligned16(o) || !aligned16(workspace) || ((uintptr_t)lse & 3u))
         return SFA_ERR_INVALID_ARGUMENT;
+    if (!uses_simt(desc)) return SFA_ERR_UNSUPPORTED;
     if (workspace_bytes < ws_bytes(desc)) return SFA_ERR_RESOURCE;
-    return run_attn(desc, q_idx, q_val, v, o, lse, workspace, (cudaStream_t)stream);
+    const AttnParams p = make_params(desc, q_idx, q_val, nullptr, nullptr, v, o, lse, workspace);
+    return from_cuda(launch_attn_simt(p, desc->dtype == SFA_BF16, desc->d, desc->d_v, (cudaStream_t)stream));
 }
 
 sfa_status sfa_attn_fwd(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val, const uint8_t *k_idx,
@@ -149,15 +195,50 @@ sfa_status sfa_attn_fwd(const sfa_attn_desc *desc, const uint8_t *q_idx, const v
                         size_t workspace_bytes, sfa_stream_t stream) {
     sfa_status s = validate_desc(desc);
     if (s != SFA_OK) return s;
-    if (!q_idx || !q_val || !k_idx || !k_val || !v || !o || !lse || !workspace) return SFA_ERR_INVALID_ARGUMENT;
-    if (!aligned16(v) || !aligned16(o) || !aligned16(workspace) || ((uintptr_t)lse & 3u))
+    if (!q_idx || !q_val || !k_idx || !k_val || !v || !o || !lse) return SFA_ERR_INVALID_ARGUMENT;
+    if (!aligned16(v) || !aligned16(o) || ((uintptr_t)lse & 3u) || !codes_aligned(q_idx, q_val) ||
+        !codes_aligned(k_idx, k_val))
         return SFA_ERR_INVALID_ARGUMENT;
     if (workspace_bytes < ws_bytes(desc)) return SFA_ERR_RESOURCE;
-    s = from_cuda(launch_bucket(k_idx, k_val, desc->dtype == SFA_BF16, desc->d, desc->k,
-                                (int64_t)desc->B * desc->H_kv, desc->n_kv, layout_of(desc), workspace,
-                                (cudaStream_t)stream));
+    if (!workspace || !aligned16(workspace)) return SFA_ERR_INVALID_ARGUMENT;
+    return run_attn(desc, q_idx, q_val, k_idx, k_val, v, o, lse, workspace, (cudaStream_t)stream);
+}
+
+sfa_status sfa_attn_prepare(const sfa_attn_desc *desc, const uint8_t *k_idx, const void *k_val, const void *v,
+                            void *workspace, size_t workspace_bytes, sfa_stream_t stream) {
+    sfa_status s = validate_desc(desc);
     if (s != SFA_OK) return s;
-    return run_attn(desc, q_idx, q_val, v, o, lse, workspace, (cudaStream_t)stream);
+    if (!k_idx || !k_val || !v || !workspace) return SFA_ERR_INVALID_ARGUMENT;
+    if (!aligned16(v) || !aligned16(workspace) || !codes_aligned(k_idx, k_val)) return SFA_ERR_INVALID_ARGUMENT;
+    if (workspace_bytes < ws_bytes(desc)) return SFA_ERR_RESOURCE;
+    return run_prepare(desc, k_idx, k_val, v, workspace, (cudaStream_t)stream);
+}
+
+sfa_status sfa_attn_fwd_prepared(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val,
+                                 const uint8_t *k_idx, const void *k_val, const void *v, void *o, float *lse,
+                                 const void *workspace, size_t workspace_bytes, sfa_stream_t stream) {
+    sfa_status s = validate_desc(desc);
+    if (s != SFA_OK) return s;
+    if (!q_idx || !q_val || !k_idx || !k_val || !v || !o || !lse || !workspace) return SFA_ERR_INVALID_ARGUMENT;
+    if (!aligned16(v) || !aligned16(o) || ((uintptr_t)lse & 3u) || !aligned16(workspace) ||
+        !codes_aligned(q_idx, q_val) || !codes_aligned(k_idx, k_val))
+        return SFA_ERR_INVALID_ARGUMENT;
+    if (workspace_bytes < ws_bytes(desc)) return SFA_ERR_RESOURCE;
+    return run_attn_prepared(desc, q_idx, q_val, k_idx, k_val, v, o, lse, (void *)workspace, (cudaStream_t)stream);
+}
+
+sfa_status sfa_debug_sm100_scores(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val,
+                                  const uint8_t *k_idx, const void *k_val, const void *v, void *o, float *lse,
+                                  void *workspace, size_t workspace_bytes, float *scores, sfa_stream_t stream) {
+    sfa_status s = validate_desc(desc);
+    if (s != SFA_OK) return s;
+    if (uses_simt(desc)) return SFA_ERR_UNSUPPORTED;
+    if (!q_idx || !q_val || !k_idx || !k_val || !v || !o || !lse || !scores || !workspace) return SFA_ERR_INVALID_ARGUMENT;
+    if (workspace_bytes < ws_bytes(desc)) return SFA_ERR_RESOURCE;
+    cudaStream_t st = (cudaStream_t)stream;
+    s = run_prepare(desc, k_idx, k_val, v, workspace, st);
+    if (s != SFA_OK) return s;
+    return run_attn_prepared(desc, q_idx, q_val, k_idx, k_val, v, o, lse, workspace, st, scores);
 }
 
 size_t sfa_forward_scratch_bytes(const sfa_attn_desc *desc) {
@@ -187,10 +268,7 @@ sfa_status sfa_forward(const sfa_attn_desc *desc, const void *q, const void *k, 
     e = launch_topk(k, bf16, (int64_t)desc->B * desc->H_kv * desc->n_kv, desc->d, desc->d, desc->k, S + L.k_idx,
                     S + L.k_val, status, st);
     if (e != cudaSuccess) return SFA_ERR_CUDA;
-    e = launch_bucket(S + L.k_idx, S + L.k_val, bf16, desc->d, desc->k, (int64_t)desc->B * desc->H_kv, desc->n_kv,
-                      layout_of(desc), S + L.ws, st);
-    if (e != cudaSuccess) return SFA_ERR_CUDA;
-    return run_attn(desc, S + L.q_idx, S + L.q_val, v, o, lse, S + L.ws, st);
+    return run_attn(desc, S + L.q_idx, S + L.q_val, S + L.k_idx, S + L.k_val, v, o, lse, S + L.ws, st);
 }
 
 sfa_status sfa_forward_host(const sfa_attn_desc *desc, const void *q_host, const void *k_host, const void *v_host,

@@ -7,7 +7,11 @@ namespace sfa {
 struct AttnParams {
     const uint8_t *q_idx;
     const void *q_val;
+    const uint8_t *k_idx;  // key codes (sm100 kernel decompresses them on chip; SIMT reads buckets)
+    const void *k_val;
     const void *v;
+    const void *v16;         // sm100: fp16 copy of V scaled by 2^-e per (b, kv head) (vprep.cu)
+    const uint32_t *v_amax;  // sm100: per (b, kv head) max|V| bits, e = vprep_head_exp(bits)
     void *o;
     float *lse;
     const uint8_t *ws;
@@ -22,8 +26,18 @@ cudaError_t launch_topk(const void *x, bool bf16, int64_t rows, int d, int64_t l
                         uint32_t *status_word, cudaStream_t stream);
 cudaError_t launch_bucket(const uint8_t *k_idx, const void *k_val, bool bf16, int d, int k, int64_t bh_kv,
                           int64_t n_kv, const BucketLayout &L, void *ws, cudaStream_t stream);
+// P.V operand prep for the sm100 kernel: amax[bh] = max|V| bits, v16 = fp16(V * 2^-e) (vprep.cu)
+cudaError_t launch_vprep(const void *v, int64_t bh_kv, int64_t n_kv, int d_v, uint32_t *amax, void *v16,
+                         cudaStream_t stream);
+// e >= 0 with max|V| * 2^-e < 2^15 (fp16-safe); shared by vprep.cu and the attention epilogue
+__device__ __forceinline__ int vprep_head_exp(uint32_t amax_bits) {
+    const int E = (int)((amax_bits >> 23) & 0xFF) - 127;
+    return E > 14 ? E - 14 : 0;
+}
 cudaError_t launch_attn_simt(const AttnParams &p, bool bf16, int d, int d_v, cudaStream_t stream);
-// sm_100a tcgen05 kernel; returns cudaErrorNotSupported for shapes it does not cover
-cudaError_t launch_attn_sm100(const AttnParams &p, int d, int d_v, cudaStream_t stream);
+// sm_100a tcgen05 kernel (bf16); returns cudaErrorNotSupported for shapes it does not cover.
+// dbg (tests only, may be null): receives the raw 128x128 fp32 score tile S = Q~ K~^T of the
+// first key tile of work item 0, query tile 0.
+cudaError_t launch_attn_sm100(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
 
 }  // namespace sfa

@@ -1,0 +1,80 @@
+// vprep.cu -- P.V operand preparation for the sm_100a kernel (reading A12).
+//
+// The tensor-core P.V takes A = P and B = V in the same 16-bit format.  Rounding P to bf16 costs
+// 2^-9 relative per weight, which alone can exceed the 2e-3 bar on |O| ~ 1 rows; fp16 P costs
+// 2^-12.  V therefore goes to fp16 too, EXACTLY: V' = V * 2^-e with one power of two per
+// (batch, kv head) chosen so max|V'| < 2^15 (bf16's 8-bit significand fits fp16's 11 bits; only
+// |V'| < 2^-14, i.e. below 2^-29 max|V|, loses bits to fp16 subnormals).  The attention epilogue
+// multiplies O by 2^e.  Two HBM-bound passes: absmax per head, then convert.
+#include <cuda_fp16.h>
+
+#include "launch.cuh"
+
+namespace sfa {
+
+namespace {
+
+// absmax of |V| per (b, kv head): float bits of a non-negative value order like unsigned ints
+__global__ void __launch_bounds__(256) v_absmax_kernel(const uint4 *__restrict__ v, int64_t vec_per_head,
+                                                        uint32_t *__restrict__ amax) {
+    const int bh = blockIdx.y;
+    const uint4 *src = v + (int64_t)bh * vec_per_head;
+    uint32_t m = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < vec_per_head;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 x = __ldg(src + i);
+        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            m = max(m, (w[e] << 16) & 0x7FFFFFFFu);
+            m = max(m, w[e] & 0x7FFF0000u);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(amax + bh, m);
+}
+
+__global__ void __launch_bounds__(256) v_to_f16_kernel(const uint4 *__restrict__ v, int64_t vec_per_head,
+                                                        const uint32_t *__restrict__ amax, uint2 *__restrict__ out) {
+    const int bh = blockIdx.y;
+    const int e = vprep_head_exp(__ldg(amax + bh));
+    const float sc = __uint_as_float((uint32_t)(127 - e) << 23);  // 2^-e, exact
+    const uint4 *src = v + (int64_t)bh * vec_per_head;
+    uint4 *dst = reinterpret_cast<uint4 *>(out) + (int64_t)bh * vec_per_head;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < vec_per_head;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 x = __ldcs(src + i);
+        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const __half2 h = __floats2half2_rn(__uint_as_float(w[q] << 16) * sc, __uint_as_float(w[q] & 0xFFFF0000u) * sc);
+            o[q] = *reinterpret_cast<const uint32_t *>(&h);
+        }
+        dst[i] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_vprep(const void *v, int64_t bh_kv, int64_t n_kv, int d_v, uint32_t *amax, void *v16,
+                         cudaStream_t stream) {
+    if (bh_kv == 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(amax, 0, (size_t)bh_kv * 4, stream);
+    if (e != cudaSuccess) return e;
+    const int64_t vec = n_kv * d_v / 8;  // 16-byte vectors per head (d_v is a multiple of 8)
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t gx = (vec + 255) / 256;
+    const int64_t cap = ((int64_t)sms * 8 + bh_kv - 1) / bh_kv;  // about 8 CTAs per SM in total
+    if (gx > cap) gx = cap;
+    if (gx < 1) gx = 1;
+    dim3 grid((unsigned)gx, (unsigned)bh_kv);
+    v_absmax_kernel<<<grid, 256, 0, stream>>>((const uint4 *)v, vec, amax);
+    v_to_f16_kernel<<<grid, 256, 0, stream>>>((const uint4 *)v, vec, amax, (uint2 *)v16);
+    return cudaGetLastError();
+}
+
+}  // namespace sfa

@@ -55,11 +55,14 @@ def lib() -> ctypes.CDLL:
             "sfa_attn_fwd": ([D, P, P, P, P, P, P, P, P, SZ, P], I32),
             "sfa_bucket_keys": ([D, P, P, P, SZ, P], I32),
             "sfa_attn_fwd_bucketed": ([D, P, P, P, P, P, P, SZ, P], I32),
+            "sfa_attn_prepare": ([D, P, P, P, P, SZ, P], I32),
+            "sfa_attn_fwd_prepared": ([D, P, P, P, P, P, P, P, P, SZ, P], I32),
             "sfa_key_tile": ([D], I32),
             "sfa_forward_scratch_bytes": ([D], SZ),
             "sfa_forward": ([D, P, P, P, P, P, P, SZ, P], I32),
             "sfa_forward_host": ([D, P, P, P, P, P, P, P, P, P, P, P, SZ, P], I32),
             "sfa_device_supported": ([], I32),
+            "sfa_debug_sm100_scores": ([D, P, P, P, P, P, P, P, P, SZ, P, P], I32),
             "sfa_gen_fill": ([P, I32, I64, I64, ctypes.c_uint64, I32, I32, I64, I32, I32, P], I32),
         }
         for name, (args, res) in sig.items():
@@ -71,7 +74,8 @@ def lib() -> ctypes.CDLL:
 
 EXPORTS = ("sfa_status_string", "sfa_topk_codes", "sfa_attn_workspace_bytes", "sfa_attn_fwd", "sfa_bucket_keys",
            "sfa_attn_fwd_bucketed", "sfa_key_tile", "sfa_forward_scratch_bytes", "sfa_forward",
-           "sfa_forward_host", "sfa_device_supported", "sfa_gen_fill")
+           "sfa_forward_host", "sfa_device_supported", "sfa_gen_fill", "sfa_debug_sm100_scores",
+           "sfa_attn_prepare", "sfa_attn_fwd_prepared")
 
 
 def _check(code: int, where: str):
@@ -159,7 +163,7 @@ def bucket_keys(k_idx, k_val, *, d, n_q=1, H=None, d_v=64, causal=True, workspac
     _dev(k_idx, k_val)
     B, H_kv, n_kv, k = k_idx.shape
     desc = make_desc(B=B, H=H or H_kv, H_kv=H_kv, d=d, k=k, d_v=d_v, n_q=n_q, n_kv=n_kv, causal=causal,
-                     dtype=_dt(k_val))
+                     dtype=_dt(k_val), kernel=KERNEL_SIMT)  # buckets feed the CUDA-core kernel
     nb = workspace_bytes(desc)
     if workspace is None:
         workspace = torch.zeros(max(nb, 16), dtype=torch.uint8, device=k_idx.device)
@@ -178,6 +182,22 @@ def attn_fwd_bucketed(desc: AttnDesc, q_idx, q_val, v, workspace, out=None):
     _check(lib().sfa_attn_fwd_bucketed(ctypes.byref(desc), _p(q_idx), _p(q_val), _p(v), _p(o), _p(lse),
                                        _p(workspace), workspace.numel(), _stream()), "sfa_attn_fwd_bucketed")
     return o, lse
+
+
+def debug_sm100_scores(q_idx, q_val, k_idx, k_val, v, *, d, causal=True, scale=None):
+    """Diagnostic: run the sm_100a kernel and return (O, LSE, S) where S [128, 128] fp32 is the raw
+    score tile Q~ K~^T of the first key tile of work item 0 / query tile 0 (include/sfa.h)."""
+    _dev(q_idx, q_val, k_idx, k_val, v)
+    desc = _desc_from_codes(q_idx, k_idx, v, d, causal, scale, 0, KERNEL_SM100, _dt(v))
+    B, H, n_q, _ = q_idx.shape
+    o = torch.empty((B, H, n_q, v.shape[-1]), dtype=v.dtype, device=v.device)
+    lse = torch.empty((B, H, n_q), dtype=torch.float32, device=v.device)
+    S = torch.full((128, 128), float("nan"), dtype=torch.float32, device=v.device)
+    ws = torch.empty(max(workspace_bytes(desc), 16), dtype=torch.uint8, device=v.device)
+    _check(lib().sfa_debug_sm100_scores(ctypes.byref(desc), _p(q_idx), _p(q_val), _p(k_idx), _p(k_val), _p(v),
+                                        _p(o), _p(lse), _p(ws), ws.numel(), _p(S), _stream()),
+           "sfa_debug_sm100_scores")
+    return o, lse, S
 
 
 def scratch_bytes(desc: AttnDesc) -> int:

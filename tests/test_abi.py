@@ -60,8 +60,11 @@ def desc(sfa, **kw):
 
 def test_desc_validation(sfa):
     L = sfa.lib()
-    ok = desc(sfa)
+    ok = desc(sfa, kernel=sfa.KERNEL_SIMT)
     assert L.sfa_attn_workspace_bytes(ctypes.byref(ok)) > 0
+    # the sm_100a kernel decompresses key codes on chip (no buckets); its workspace is the
+    # 256-aligned max|V| per (b, kv head) + the fp16 copy of V (reading A12)
+    assert L.sfa_attn_workspace_bytes(ctypes.byref(desc(sfa))) == 256 + 1 * 2 * 300 * 128 * 2
     bad = [dict(H=3, H_kv=2), dict(k=0), dict(k=129), dict(n_q=0), dict(n_kv=0), dict(scale=-1.0),
            dict(scale=float("inf")), dict(q_pos0=-1)]
     for b in bad:
@@ -83,10 +86,18 @@ def test_workspace_layout(sfa):
     L = sfa.lib()
     for (k, bk) in ((8, 128), (16, 128), (32, 128), (64, 64), (128, 64)):
         for dt, eb in ((sfa.SFA_BF16, 4), (sfa.SFA_F32, 8)):
-            d = desc(sfa, k=k, dtype=dt)
+            d = desc(sfa, k=k, dtype=dt, kernel=sfa.KERNEL_SIMT)
             assert L.sfa_key_tile(ctypes.byref(d)) == bk
             off = (129 * 2 + 15) // 16 * 16
             cap = (bk * k + 3 * 128 + 3) // 4 * 4
             tile = (off + cap * eb + 15) // 16 * 16
             ntiles = (300 + bk - 1) // bk
             assert L.sfa_attn_workspace_bytes(ctypes.byref(d)) == 1 * 2 * ntiles * tile
+
+
+def test_bucketed_entry_points_need_simt(sfa):
+    """sfa_bucket_keys / sfa_attn_fwd_bucketed feed the CUDA-core kernel only (unsupported otherwise)."""
+    L = sfa.lib()
+    d = desc(sfa, kernel=sfa.KERNEL_SM100)
+    assert L.sfa_bucket_keys(ctypes.byref(d), *([ctypes.c_void_p(16)] * 3), 1 << 30, None) == 3
+    assert L.sfa_attn_fwd_bucketed(ctypes.byref(d), *([ctypes.c_void_p(16)] * 6), 1 << 30, None) == 3

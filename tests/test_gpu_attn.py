@@ -14,7 +14,7 @@ from paper_2603_22300_b200 import inputs
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = {"simt": 1, "auto": 0}
+KERNELS = {"simt": 1, "sm100": 2}  # "auto" = sm100 for bf16, simt for fp32 (test_forward_*)
 
 
 def gpu_attn(lib, qi, qv, ki, kv, v, dtype, d, **kw):
@@ -38,6 +38,8 @@ def run_case(lib, seed, B, H, H_kv, n, d, d_v, k, dtype, causal=True, variant="i
 @pytest.mark.parametrize("kernel", list(KERNELS))
 def test_tiny_config(lib, kernel):
     """BASELINE configs[0]: B=1,H=1,n=256,d=64,k=8, causal, fp32 -> 1e-5 relative."""
+    if kernel == "sm100":
+        pytest.skip("fp32 runs on the CUDA-core kernel only (reading A12)")
     for seed in (1, 2, 3):
         run_case(lib, seed, 1, 1, 1, 256, 64, 64, 8, "f32", kernel=KERNELS[kernel])
     run_case(lib, 2, 1, 1, 1, 256, 64, 64, 8, "f32", variant="lattice", kernel=KERNELS[kernel])
