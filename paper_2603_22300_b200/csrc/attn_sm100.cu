@@ -149,6 +149,21 @@ __device__ __forceinline__ void densify_row(uint32_t tile, int rows, int r, bool
     }
 }
 
+// Debug timeline (build with SFA_NVCC_FLAGS=-DSFA_TIMELINE): CTA 0 appends (tag, clock64) records
+// after the score tile in the diagnostic buffer of sfa_debug_sm100_scores.
+#ifdef SFA_TIMELINE
+#define TLREC(tag)                                                                                   \
+    do {                                                                                             \
+        if (a.dbg != nullptr && blockIdx.x == 0) {                                                   \
+            unsigned long long *tb_ = reinterpret_cast<unsigned long long *>(a.dbg + BM * BN);       \
+            const unsigned i_ = atomicAdd(reinterpret_cast<unsigned *>(tb_), 1u);                    \
+            if (i_ < 8000) tb_[1 + i_] = ((unsigned long long)(tag) << 48) | (clock64() & 0xFFFFFFFFFFFFull); \
+        }                                                                                            \
+    } while (0)
+#else
+#define TLREC(tag) do {} while (0)
+#endif
+
 template <int D, int DV>
 __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_kernel(const __grid_constant__ CUtensorMap tmap_v,
                                                                    const Sm100Args a) {
@@ -208,6 +223,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_kernel(const __grid_co
         float m = -INFINITY, l = 0.f;
         for (int j = 0; j < nt; ++j) {
             mbar_wait(BAR(SFULL + t), j & 1);
+            if (lane == 0 && wq == 0) TLREC(0x1000 | (t << 10) | (j & 1023));
             tc_fence_after();
             uint32_t s[4][32];
 #pragma unroll
@@ -273,6 +289,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_kernel(const __grid_co
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(BAR(PFULL + t));
+            if (lane == 0 && wq == 0) TLREC(0x2000 | (t << 10) | (j & 1023));
         }
         // ---- epilogue (step 8)
         mbar_wait(BAR(OFULL), 0);
@@ -365,6 +382,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_kernel(const __grid_co
                     const int s1 = (j + 1) & 1, u1 = (j + 1) >> 1;
                     mbar_wait(BAR(VFULL + s), u & 1);
                     mbar_wait(BAR(PFULL + 0), j & 1);
+                    TLREC(0x3000 | (j & 1023));
                     tc_fence_after();
                     mma_O(0, s, j > 0);
                     if (nxt) {
@@ -374,6 +392,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_kernel(const __grid_co
                         umma_commit(BAR(SFULL + 0));
                     }
                     mbar_wait(BAR(PFULL + 1), j & 1);
+                    TLREC(0x3400 | (j & 1023));
                     tc_fence_after();
                     mma_O(1, s, j > 0);
                     umma_commit(BAR(VEMPTY + s));

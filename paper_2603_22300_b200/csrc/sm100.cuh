@@ -6,6 +6,7 @@
 #pragma once
 #include <cuda.h>
 #include <stdint.h>
+#include <stdio.h>
 
 namespace sfa {
 namespace sm100 {
@@ -27,6 +28,7 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
 }
 // Wait until the phase with the given parity has completed.  On a freshly initialised barrier,
 // parity 1 returns immediately (the "previous" phase counts as complete): producers start there.
+#ifndef SFA_WATCHDOG
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -36,6 +38,25 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+#else
+// debug build (SFA_NVCC_FLAGS=-DSFA_WATCHDOG): a wait that spins too long reports itself and traps
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    for (long long it = 0;; ++it) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (it == (1ll << 22)) {
+            printf("sfa watchdog: block %d thread %d waits bar@%u parity %u\n", blockIdx.x, threadIdx.x, bar & 0xFFFF,
+                   parity);
+            __trap();
+        }
+    }
+}
+#endif
 
 // ---- proxies / fences --------------------------------------------------------------------------
 // generic-proxy smem writes -> visible to the async proxy (tcgen05.mma operand reads, TMA)

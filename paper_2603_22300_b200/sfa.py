@@ -192,12 +192,14 @@ def debug_sm100_scores(q_idx, q_val, k_idx, k_val, v, *, d, causal=True, scale=N
     B, H, n_q, _ = q_idx.shape
     o = torch.empty((B, H, n_q, v.shape[-1]), dtype=v.dtype, device=v.device)
     lse = torch.empty((B, H, n_q), dtype=torch.float32, device=v.device)
-    S = torch.full((128, 128), float("nan"), dtype=torch.float32, device=v.device)
+    # score tile [128 x 128] fp32, then room for the debug-build timeline (SFA_TIMELINE)
+    S = torch.full((128 * 128 + 2 * 8192,), float("nan"), dtype=torch.float32, device=v.device)
+    S[128 * 128:] = 0
     ws = torch.empty(max(workspace_bytes(desc), 16), dtype=torch.uint8, device=v.device)
     _check(lib().sfa_debug_sm100_scores(ctypes.byref(desc), _p(q_idx), _p(q_val), _p(k_idx), _p(k_val), _p(v),
                                         _p(o), _p(lse), _p(ws), ws.numel(), _p(S), _stream()),
            "sfa_debug_sm100_scores")
-    return o, lse, S
+    return o, lse, S[:128 * 128].view(128, 128), S[128 * 128:]
 
 
 def scratch_bytes(desc: AttnDesc) -> int:

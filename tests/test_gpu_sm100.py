@@ -32,7 +32,7 @@ def test_score_tile_is_exact_overlap_sum(lib, d, k):
     q, kx, v = host_qkv(101 + k, B, H, H_kv, n, d, d_v, "bf16")
     qi, qv = oracle_codes(q, k)
     ki, kv = oracle_codes(kx, k)
-    o, lse, S = lib.debug_sm100_scores(to_torch(qi, "u8"), to_torch(qv, "bf16"), to_torch(ki, "u8"),
+    o, lse, S, _ = lib.debug_sm100_scores(to_torch(qi, "u8"), to_torch(qv, "bf16"), to_torch(ki, "u8"),
                                        to_torch(kv, "bf16"), to_torch(v, "bf16"), d=d)
     torch.cuda.synchronize()
     S = S.cpu().numpy().astype(np.float64)

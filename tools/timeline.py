@@ -1,0 +1,47 @@
+"""Hand-off timeline of the sm100 kernel's CTA 0 (library built with SFA_NVCC_FLAGS=-DSFA_TIMELINE).
+
+Runs one non-causal forward whose work item 0 has NT key tiles and prints, per 64-key sub-tile u,
+when each softmax group saw S(u) ready and stored P(u), and when the MMA warp saw P(u)."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2603_22300_b200 import inputs, sfa  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+B, H, H_kv, d, d_v, k = 1, 2, 1, 128, 128, 16
+dev = "cuda"
+Q = sfa.gen_fill(torch.empty((B, H, n, d), dtype=torch.bfloat16, device=dev), 3, inputs.TID_Q)
+K = sfa.gen_fill(torch.empty((B, H_kv, n, d), dtype=torch.bfloat16, device=dev), 3, inputs.TID_K)
+V = sfa.gen_fill(torch.empty((B, H_kv, n, d_v), dtype=torch.bfloat16, device=dev), 3, inputs.TID_V)
+qi, qv = sfa.topk_codes(Q, k)
+ki, kv = sfa.topk_codes(K, k)
+for _ in range(2):
+    o, lse, S, tlb = sfa.debug_sm100_scores(qi, qv, ki, kv, V, d=d, causal=False)
+torch.cuda.synchronize()
+raw = tlb.cpu().numpy().view(np.uint64)
+cnt = int(raw[0] & np.uint64(0xFFFFFFFF))
+rec = raw[1:1 + cnt]
+tag = (rec >> np.uint64(48)).astype(np.int64)
+clk = (rec & np.uint64(0xFFFFFFFFFFFF)).astype(np.int64)
+clk -= clk.min()
+names = {1: "S_ready", 2: "P_stored", 3: "mma_sawP"}
+ev = {}
+for tg, c in zip(tag, clk):
+    kind, t, u = tg >> 12, (tg >> 10) & 3, tg & 1023
+    ev[(names[kind], t, u)] = c
+nu = max(u for (_, _, u) in ev) + 1
+print(f"{cnt} records, {nu} key tiles; clocks relative to the first record")
+print(" j | S0rdy  P0st  mmaP0 | S1rdy  P1st  mmaP1 | softmax0 softmax1 | period(S0rdy)")
+prev = None
+for u in range(nu):
+    row = [ev.get(("S_ready", 0, u), -1), ev.get(("P_stored", 0, u), -1), ev.get(("mma_sawP", 0, u), -1),
+           ev.get(("S_ready", 1, u), -1), ev.get(("P_stored", 1, u), -1), ev.get(("mma_sawP", 1, u), -1)]
+    per = row[0] - prev if prev is not None else 0
+    prev = row[0]
+    print(f"{u:3d} | {row[0]:6d} {row[1]:6d} {row[2]:6d} | {row[3]:6d} {row[4]:6d} {row[5]:6d} | "
+          f"{row[1]-row[0]:6d} {row[4]-row[3]:6d} | {per}")
