@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--k", type=int, default=None, help="override the code size k (sweep)")
+    ap.add_argument("--shard-seq", action="store_true",
+                    help="query-block sharding of one sequence (default for --config long under torchrun, N>1; "
+                         "with N=1 it exercises the same NCCL path on one GPU)")
     return ap.parse_args()
 
 
@@ -186,6 +189,119 @@ L2_FLUSH_MB = 512
 
 
 # --------------------------------------------------------------------------------------------
+def run_sharded(args, W, rank, world, local):
+    """Long-context query-block sharding: one sequence of n tokens over `world`
+    GPUs, zig-zag chunks, one NCCL all-gather of key codes + V per step (strong scaling)."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_22300_b200 import dist as sdist
+    from paper_2603_22300_b200 import inputs, sfa
+    dev = torch.device("cuda", local)
+    B, H, H_kv, n, d, d_v, k = W.B, W.H, W.H_kv, W.n, W.d, W.d_v, W.k
+    c = sdist.chunk_size(n, world)
+    chunks = sdist.owned_chunks(rank, world)
+    seed = accounting.SEEDS[args.config]
+    bf = torch.bfloat16
+
+    def local_fill(hh, dd, tid):  # chunk-major [2][B][hh][c][dd] slice of the global [B][hh][n][dd] tensor
+        t = torch.empty((2, B, hh, c, dd), dtype=bf, device=dev)
+        for half, q in enumerate(chunks):
+            for b in range(B):
+                for h in range(hh):
+                    sfa.gen_fill(t[half, b, h], seed, tid, offset=((b * hh + h) * n + q * c) * dd)
+        return t
+
+    Q, K, V = local_fill(H, d, inputs.TID_Q), local_fill(H_kv, d, inputs.TID_K), local_fill(H_kv, d_v, inputs.TID_V)
+    sh = sdist.ShardedAttention()
+    L = sfa.lib()
+    P_ = lambda t: ctypes.c_void_p(t.data_ptr())
+    st = lambda: ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    qi = torch.empty((2, B, H, c, k), dtype=torch.uint8, device=dev)
+    qv = torch.empty((2, B, H, c, k), dtype=bf, device=dev)
+    ki = torch.empty((2, B, H_kv, c, k), dtype=torch.uint8, device=dev)
+    kv = torch.empty((2, B, H_kv, c, k), dtype=bf, device=dev)
+    kfi = torch.empty((B, H_kv, n, k), dtype=torch.uint8, device=dev)
+    kfv = torch.empty((B, H_kv, n, k), dtype=bf, device=dev)
+    vf = torch.empty((B, H_kv, n, d_v), dtype=bf, device=dev)
+    ldesc = sfa.make_desc(B=B, H=H_kv, H_kv=H_kv, d=d, k=k, d_v=d_v, n_q=2 * c, n_kv=2 * c)
+    nst = int(L.sfa_dist_staging_bytes(ctypes.byref(ldesc), world))
+    staging = torch.empty(nst, dtype=torch.uint8, device=dev)
+    desc = sfa.make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k, d_v=d_v, n_q=c, n_kv=n, causal=W.causal)
+    ws = torch.empty(max(sfa.workspace_bytes(desc), 16), dtype=torch.uint8, device=dev)
+    O = torch.empty((2, B, H, c, d_v), dtype=bf, device=dev)
+    LSE = torch.empty((2, B, H, c), dtype=torch.float32, device=dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    flush = torch.empty(L2_FLUSH_MB * 2 ** 20, dtype=torch.uint8, device=dev)
+
+    def step(ev=None):
+        if ev: ev[0].record()
+        r = [L.sfa_topk_codes(P_(Q), sfa.SFA_BF16, 2 * B * H * c, d, d, k, P_(qi), P_(qv), P_(status), st()),
+             L.sfa_topk_codes(P_(K), sfa.SFA_BF16, 2 * B * H_kv * c, d, d, k, P_(ki), P_(kv), P_(status), st())]
+        if ev: ev[1].record()
+        r.append(L.sfa_dist_allgather_kv(sh._h, ctypes.byref(ldesc), P_(ki), P_(kv), P_(V), P_(kfi), P_(kfv), P_(vf),
+                                         P_(staging), nst, st()))
+        if ev: ev[2].record()
+        r.append(L.sfa_attn_prepare(ctypes.byref(desc), P_(kfi), P_(kfv), P_(vf), P_(ws), ws.numel(), st()))
+        if ev: ev[3].record()
+        for half, q in enumerate(chunks):
+            desc.q_pos0 = q * c
+            r.append(L.sfa_attn_fwd_prepared(ctypes.byref(desc), P_(qi[half]), P_(qv[half]), P_(kfi), P_(kfv),
+                                             P_(vf), P_(O[half]), P_(LSE[half]), P_(ws), ws.numel(), st()))
+        if ev: ev[4].record()
+        if any(r):
+            raise RuntimeError(f"sfa call failed: {r}")
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            step(evs[i])
+        torch.cuda.synchronize()
+    dist.barrier()
+    per = [[e[j].elapsed_time(e[j + 1]) for j in range(4)] for e in evs]
+    tot = torch.tensor([sum(sum(p) for p in per)], dtype=torch.float64, device=dev)
+    dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms = float(tot.item()) / args.steps
+    stage = [sum(p[j] for p in per) / args.steps for j in range(4)]
+    attn_ms = torch.tensor([stage[3]], dtype=torch.float64, device=dev)
+    dist.all_reduce(attn_ms, op=dist.ReduceOp.MAX)
+    pairs_rank = B * H * sdist.causal_pairs_of_rank(rank, world, n)
+    pk = peaks()
+    mufu_peak = N_SMS * MUFU_EX2_PER_CLK_SM * pk["sm_max_mhz"] * 1e6
+    achieved = pairs_rank / (float(attn_ms.item()) / 1e3)
+    ag_bytes = world * (ki.numel() + kv.numel() * 2 + V.numel() * 2)
+    sh.close()
+    if rank == 0:
+        line = {"metric": METRIC, "value": B * n / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (seeded counter-based generator on device, DESIGN.md input recipe)",
+                "config": {"workload": f"long: B={B}, H={H}, H_kv={H_kv}, n={n}, d={d}, d_v={d_v}, k={k}, causal, "
+                                       f"bf16 V; one sequence sharded over {world} GPUs",
+                           "global_batch": B, "seq_len": n,
+                           "parallelism": f"zig-zag query blocks x{world} (chunks p, 2P-1-p of {c} tokens), "
+                                          "one NCCL all-gather of key codes + V per step",
+                           "l2": f"explicit {L2_FLUSH_MB} MB write between timed steps"},
+                "stage_ms": {"topk_qk": stage[0], "allgather_kv": stage[1], "prepare": stage[2], "attn": stage[3]},
+                "allgather_bytes_per_rank": ag_bytes,
+                "roofline": {"bound": "alu", "kernel": "attn_sm100_kernel (steps 4-8), per rank",
+                             "achieved": achieved / 1e9, "peak": mufu_peak / 1e9,
+                             "unit": "G pairs/s (1 MUFU ex2 per allowed causal pair)", "frac": achieved / mufu_peak,
+                             "traffic": None, "peak_source": "148 SMs x 16 ex2/clk x max SM clock"},
+                "cpu_baseline": None, "e2e": None,
+                "gpu_launches": 9 * args.steps, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     W = accounting.CONFIGS[args.config]
@@ -202,6 +318,14 @@ def main():
 
     from paper_2603_22300_b200 import inputs, sfa
     torch.cuda.set_device(local)
+    if args.shard_seq or (args.config == "long" and world > 1):
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
+        run_sharded(args, W, rank, world, local)
+        dist.destroy_process_group()
+        return
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     kernel = {"auto": sfa.KERNEL_AUTO, "simt": sfa.KERNEL_SIMT, "sm100": sfa.KERNEL_SM100}[args.kernel]

@@ -166,6 +166,37 @@ SFA_API sfa_status sfa_debug_sm100_scores(const sfa_attn_desc *desc, const uint8
                                           float *lse, void *workspace, size_t workspace_bytes, float *scores,
                                           sfa_stream_t stream);
 
+/* ------------------------------------------------------------------------------------------
+ * Step 9 (sharded path only): query-block sharding of one sequence over P GPUs.
+ * Zig-zag partition: the sequence is cut into 2P chunks of c tokens; rank p owns chunks p and
+ * 2P-1-p (equal causal work), held chunk-major as [2][B][H(_kv)][c][.] (chunk p, then chunk
+ * 2P-1-p), so each query chunk's codes and outputs are contiguous.
+ * NCCL is loaded at run time (dlopen "libnccl.so.2"); without it these return SFA_ERR_UNSUPPORTED.
+ *   sfa_dist_unique_id  -- rank 0 creates the 128-byte ncclUniqueId (shared by the caller, e.g. via
+ *                          torch.distributed.broadcast_object_list);
+ *   sfa_dist_init       -- every rank joins; the handle owns the communicator (sfa_dist_destroy).
+ *   sfa_dist_allgather_kv -- local_desc describes the LOCAL keys (n_kv = 2c, even; B, H_kv, k, d_v,
+ *                          dtype as in the full problem); gathers every
+ *                          rank's key codes and V (one grouped NCCL all-gather, staged in
+ *                          `staging` >= sfa_dist_staging_bytes) and unpacks them into sequence
+ *                          order: k_idx_full [B][H_kv][2Pc][k], k_val_full, v_full [B][H_kv][2Pc][d_v].
+ *                          The caller then runs sfa_attn_fwd for each of its two query chunks with
+ *                          q_pos0 = chunk start over the full keys (reading A9).  Stream-ordered.
+ *   sfa_dist_unpack_zigzag -- the unpack alone (device buffers; rank-major [P][2][bh][chunk][row_bytes]
+ *                          -> [bh][2P][chunk][row_bytes]); used by sfa_dist_allgather_kv, exposed for tests.
+ * ------------------------------------------------------------------------------------------ */
+typedef struct sfa_dist *sfa_dist_t;
+SFA_API sfa_status sfa_dist_unique_id(void *nccl_unique_id_out /* 128 B */);
+SFA_API sfa_status sfa_dist_init(int rank, int world, const void *nccl_unique_id, sfa_dist_t *out);
+SFA_API sfa_status sfa_dist_destroy(sfa_dist_t h);
+SFA_API size_t sfa_dist_staging_bytes(const sfa_attn_desc *local_desc, int32_t world);
+SFA_API sfa_status sfa_dist_allgather_kv(sfa_dist_t h, const sfa_attn_desc *local_desc, const uint8_t *k_idx_local,
+                                         const void *k_val_local, const void *v_local, uint8_t *k_idx_full,
+                                         void *k_val_full, void *v_full, void *staging, size_t staging_bytes,
+                                         sfa_stream_t stream);
+SFA_API sfa_status sfa_dist_unpack_zigzag(const void *in, void *out, int32_t world, int64_t bh, int64_t chunk,
+                                          int64_t row_bytes, sfa_stream_t stream);
+
 /* Build / device info: 1 if the calling thread's current device is sm_100 and the kernels load. */
 SFA_API int32_t sfa_device_supported(void);
 

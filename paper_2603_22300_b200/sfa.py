@@ -56,6 +56,12 @@ def lib() -> ctypes.CDLL:
             "sfa_bucket_keys": ([D, P, P, P, SZ, P], I32),
             "sfa_attn_fwd_bucketed": ([D, P, P, P, P, P, P, SZ, P], I32),
             "sfa_attn_prepare": ([D, P, P, P, P, SZ, P], I32),
+            "sfa_dist_unique_id": ([P], I32),
+            "sfa_dist_init": ([I32, I32, P, P], I32),
+            "sfa_dist_destroy": ([P], I32),
+            "sfa_dist_staging_bytes": ([D, I32], SZ),
+            "sfa_dist_allgather_kv": ([P, D, P, P, P, P, P, P, P, SZ, P], I32),
+            "sfa_dist_unpack_zigzag": ([P, P, I32, I64, I64, I64, P], I32),
             "sfa_attn_fwd_prepared": ([D, P, P, P, P, P, P, P, P, SZ, P], I32),
             "sfa_key_tile": ([D], I32),
             "sfa_forward_scratch_bytes": ([D], SZ),
@@ -75,7 +81,8 @@ def lib() -> ctypes.CDLL:
 EXPORTS = ("sfa_status_string", "sfa_topk_codes", "sfa_attn_workspace_bytes", "sfa_attn_fwd", "sfa_bucket_keys",
            "sfa_attn_fwd_bucketed", "sfa_key_tile", "sfa_forward_scratch_bytes", "sfa_forward",
            "sfa_forward_host", "sfa_device_supported", "sfa_gen_fill", "sfa_debug_sm100_scores",
-           "sfa_attn_prepare", "sfa_attn_fwd_prepared")
+           "sfa_attn_prepare", "sfa_attn_fwd_prepared", "sfa_dist_unique_id", "sfa_dist_init", "sfa_dist_destroy",
+           "sfa_dist_staging_bytes", "sfa_dist_allgather_kv", "sfa_dist_unpack_zigzag")
 
 
 def _check(code: int, where: str):
