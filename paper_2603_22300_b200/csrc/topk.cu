@@ -107,6 +107,122 @@ __global__ void __launch_bounds__(256) topk_codes_kernel(const Bits *__restrict_
     if (status_word != nullptr && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status_word, 1u);
 }
 
+// ---------------------------------------------------------------------------------------------
+// bf16 rows: one THREAD per row (the warp-per-row kernel above issues ~500 warp instructions per
+// row and is ALU-bound at ~9% of HBM bandwidth).  A CTA of 128 threads owns 128 consecutive rows:
+//   1. coalesced 16-byte loads of the rows into shared memory, 16-byte chunks XOR-swizzled by
+//      (row & 15) so each thread then reads its own row with conflict-free LDS.128;
+//   2. the row as 64 (d=128) or 32 (d=64) registers of two bf16 each; kh = bits | 0x80008000
+//      holds both 15-bit magnitude keys with a guard bit, so (kh - T*0x10001) has bit 15 / 31 set
+//      exactly when key >= T (no borrow crosses the halves);
+//   3. the same bitwise binary search for the k-th largest key T (15 steps), counting with
+//      one subtract + mask + popc per 4 keys;
+//   4. keys > T, then ties == T lowest index first (A2), in ascending feature order (A4), staged
+//      in shared memory and written out with coalesced stores.
+// Non-finite inputs: max key (max.u16x2) >= 0x7F80.
+constexpr int TK_ROWS = 128;
+
+template <int D>
+__global__ void __launch_bounds__(TK_ROWS) topk_rows_bf16_kernel(const uint16_t *__restrict__ x, int64_t rows,
+                                                                 int64_t ld, int k, uint8_t *__restrict__ idx,
+                                                                 uint16_t *__restrict__ val,
+                                                                 uint32_t *status_word) {
+    constexpr int NW = D / 2;     // u32 words per row
+    constexpr int NC = D / 8;     // 16-byte chunks per row
+    extern __shared__ __align__(16) uint8_t sm[];
+    uint8_t *rowbuf = sm;                                   // [TK_ROWS][D*2] swizzled
+    uint8_t *oidx = sm + TK_ROWS * D * 2;                   // [TK_ROWS][k]
+    uint16_t *oval = reinterpret_cast<uint16_t *>(oidx + ((TK_ROWS * k + 15) & ~15));  // [TK_ROWS][k]
+    const int t = threadIdx.x;
+    const int64_t row0 = (int64_t)blockIdx.x * TK_ROWS;
+    const int nrows = (int)((rows - row0) < TK_ROWS ? (rows - row0) : TK_ROWS);
+
+    // 1. coalesced loads (16 B per thread per step), swizzled stores
+    for (int v = t; v < nrows * NC; v += TK_ROWS) {
+        const int r = v / NC, c = v % NC;
+        const uint4 w = __ldcs(reinterpret_cast<const uint4 *>(x + (row0 + r) * ld) + c);
+        *reinterpret_cast<uint4 *>(rowbuf + r * D * 2 + ((c ^ (r & 15) & (NC - 1)) << 4)) = w;
+    }
+    __syncthreads();
+
+    const bool active = t < nrows;
+    uint32_t kh[NW];
+    uint32_t mx2 = 0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const uint4 w = *reinterpret_cast<const uint4 *>(rowbuf + t * D * 2 + ((c ^ (t & 15) & (NC - 1)) << 4));
+        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            kh[4 * c + e] = ww[e] | 0x80008000u;
+            uint32_t m;
+            asm("max.u16x2 %0, %1, %2;" : "=r"(m) : "r"(mx2), "r"(ww[e] & 0x7FFF7FFFu));
+            mx2 = m;
+        }
+    }
+    const uint32_t mx = max(mx2 & 0xFFFFu, mx2 >> 16);
+    if (active && mx >= 0x7F80u && status_word != nullptr) atomicOr(status_word, 1u);
+
+    // #{key >= T} over the row
+    auto count_ge = [&](uint32_t T) {
+        const uint32_t t2 = T * 0x10001u;
+        int cnt = 0;
+#pragma unroll
+        for (int i = 0; i < NW; i += 2) {
+            const uint32_t a = (kh[i] - t2) & 0x80008000u, b = (kh[i + 1] - t2) & 0x80008000u;
+            cnt += __popc((a >> 1) | b);
+        }
+        return cnt;
+    };
+    // 3. largest T with #{key >= T} >= k
+    uint32_t T = 0;
+#pragma unroll 1
+    for (int bit = 14; bit >= 0; --bit) {
+        const uint32_t cand = T | (1u << bit);
+        if (count_ge(cand) >= k) T = cand;
+    }
+    int ties = k - count_ge(T + 1);  // >= 1 ties at T to take, lowest index first
+    // 4. ascending compaction into the staging area
+    uint8_t *my_i = oidx + t * k;
+    uint16_t *my_v = oval + t * k;
+    int pos = 0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const uint4 w = *reinterpret_cast<const uint4 *>(rowbuf + t * D * 2 + ((c ^ (t & 15) & (NC - 1)) << 4));
+        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const uint32_t bits = (ww[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+            const uint32_t key = bits & 0x7FFFu;
+            const bool tie = key == T;
+            const bool sel = key > T || (tie && ties > 0);
+            ties -= (tie && sel) ? 1 : 0;
+            if (sel && active) {
+                my_i[pos] = (uint8_t)(8 * c + e);
+                my_v[pos] = (uint16_t)bits;
+            }
+            pos += sel ? 1 : 0;
+        }
+    }
+    __syncthreads();
+    // coalesced copy-out of the CTA's contiguous [nrows][k] index and value blocks
+    const int nib = nrows * k;
+    uint8_t *gi = idx + row0 * k;
+    uint16_t *gv = val + row0 * k;
+    if ((k & 15) == 0) {
+        for (int v = t; v < nib / 16; v += TK_ROWS)
+            reinterpret_cast<uint4 *>(gi)[v] = reinterpret_cast<const uint4 *>(oidx)[v];
+    } else {
+        for (int v = t; v < nib; v += TK_ROWS) gi[v] = oidx[v];
+    }
+    if ((k & 7) == 0) {
+        for (int v = t; v < nib / 8; v += TK_ROWS)
+            reinterpret_cast<uint4 *>(gv)[v] = reinterpret_cast<const uint4 *>(oval)[v];
+    } else {
+        for (int v = t; v < nib; v += TK_ROWS) gv[v] = oval[v];
+    }
+}
+
 // host launcher (called from api.cu after validation)
 cudaError_t launch_topk(const void *x, bool bf16, int64_t rows, int d, int64_t ld, int k, uint8_t *idx, void *val,
                         uint32_t *status_word, cudaStream_t stream) {
@@ -118,7 +234,23 @@ cudaError_t launch_topk(const void *x, bool bf16, int64_t rows, int d, int64_t l
     const int64_t want = (rows + 7) / 8;
     const int grid = (int)(want < (int64_t)sms * 16 ? want : (int64_t)sms * 16);
     if (bf16) {
-        if (d == 64)
+        // row-per-thread kernel; 16-byte row loads need ld*2 % 16 == 0 (else the warp-per-row kernel)
+        if ((ld * 2) % 16 == 0 && ((uintptr_t)x & 15u) == 0 && ((uintptr_t)idx & 15u) == 0 &&
+            ((uintptr_t)val & 15u) == 0) {
+            const int64_t blocks = (rows + TK_ROWS - 1) / TK_ROWS;
+            const size_t smem = (size_t)TK_ROWS * d * 2 + ((TK_ROWS * k + 15) & ~15) + (size_t)TK_ROWS * k * 2;
+            if (d == 64) {
+                auto kern = topk_rows_bf16_kernel<64>;
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                kern<<<(unsigned)blocks, TK_ROWS, smem, stream>>>((const uint16_t *)x, rows, ld, k, idx,
+                                                                  (uint16_t *)val, status_word);
+            } else {
+                auto kern = topk_rows_bf16_kernel<128>;
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                kern<<<(unsigned)blocks, TK_ROWS, smem, stream>>>((const uint16_t *)x, rows, ld, k, idx,
+                                                                  (uint16_t *)val, status_word);
+            }
+        } else if (d == 64)
             topk_codes_kernel<uint16_t, 64><<<grid, 256, 0, stream>>>((const uint16_t *)x, rows, ld, k, idx,
                                                                      (uint16_t *)val, status_word);
         else
