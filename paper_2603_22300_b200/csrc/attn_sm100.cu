@@ -152,12 +152,13 @@ __device__ __forceinline__ void densify_row(uint32_t tile, int rows, int r, bool
 // Debug timeline (build with SFA_NVCC_FLAGS=-DSFA_TIMELINE): CTA 0 appends (tag, clock64) records
 // after the score tile in the diagnostic buffer of sfa_debug_sm100_scores.
 #ifdef SFA_TIMELINE
+// slot = (kind-1) * 2048 + group * 1024 + j: a plain store, no atomic on the critical path
 #define TLREC(tag)                                                                                   \
     do {                                                                                             \
         if (a.dbg != nullptr && blockIdx.x == 0) {                                                   \
             unsigned long long *tb_ = reinterpret_cast<unsigned long long *>(a.dbg + BM * BN);       \
-            const unsigned i_ = atomicAdd(reinterpret_cast<unsigned *>(tb_), 1u);                    \
-            if (i_ < 8000) tb_[1 + i_] = ((unsigned long long)(tag) << 48) | (clock64() & 0xFFFFFFFFFFFFull); \
+            const unsigned slot_ = ((((tag) >> 12) - 1) << 11) | ((tag) & 2047);                    \
+            if (slot_ < 8191) tb_[1 + slot_] = ((unsigned long long)(tag) << 48) | (clock64() & 0xFFFFFFFFFFFFull); \
         }                                                                                            \
     } while (0)
 #else

@@ -24,8 +24,9 @@ for _ in range(2):
     o, lse, S, tlb = sfa.debug_sm100_scores(qi, qv, ki, kv, V, d=d, causal=False)
 torch.cuda.synchronize()
 raw = tlb.cpu().numpy().view(np.uint64)
-cnt = int(raw[0] & np.uint64(0xFFFFFFFF))
-rec = raw[1:1 + cnt]
+rec = raw[1:]
+rec = rec[rec != 0]
+cnt = len(rec)
 tag = (rec >> np.uint64(48)).astype(np.int64)
 clk = (rec & np.uint64(0xFFFFFFFFFFFF)).astype(np.int64)
 clk -= clk.min()
@@ -36,7 +37,7 @@ for tg, c in zip(tag, clk):
     ev[(names[kind], t, u)] = c
 nu = max(u for (_, _, u) in ev) + 1
 print(f"{cnt} records, {nu} key tiles; clocks relative to the first record")
-print(" j | S0rdy  P0st  mmaP0 | S1rdy  P1st  mmaP1 | softmax0 softmax1 | period(S0rdy)")
+print(" j | S0rdy  P0st  mmaP  | S1rdy  P1st  issued | softmax0 softmax1 | period(S0rdy)")
 prev = None
 for u in range(nu):
     row = [ev.get(("S_ready", 0, u), -1), ev.get(("P_stored", 0, u), -1), ev.get(("mma_sawP", 0, u), -1),
