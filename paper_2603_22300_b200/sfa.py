@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libsfa.so")
 
 SFA_F32, SFA_BF16 = 0, 1
-KERNEL_AUTO, KERNEL_SIMT, KERNEL_SM100 = 0, 1, 2
+KERNEL_AUTO, KERNEL_SIMT, KERNEL_SM100, KERNEL_SM100_PAIR = 0, 1, 2, 3
 GEN_IID, GEN_LATTICE, GEN_SKEWED = 0, 1, 2
 _STATUS = {0: "ok", 1: "invalid-argument", 2: "invalid-input", 3: "unsupported", 4: "resource-limit",
            5: "cuda-error"}
@@ -191,11 +191,11 @@ def attn_fwd_bucketed(desc: AttnDesc, q_idx, q_val, v, workspace, out=None):
     return o, lse
 
 
-def debug_sm100_scores(q_idx, q_val, k_idx, k_val, v, *, d, causal=True, scale=None):
+def debug_sm100_scores(q_idx, q_val, k_idx, k_val, v, *, d, causal=True, scale=None, kernel=KERNEL_SM100):
     """Diagnostic: run the sm_100a kernel and return (O, LSE, S) where S [128, 128] fp32 is the raw
     score tile Q~ K~^T of the first key tile of work item 0 / query tile 0 (include/sfa.h)."""
     _dev(q_idx, q_val, k_idx, k_val, v)
-    desc = _desc_from_codes(q_idx, k_idx, v, d, causal, scale, 0, KERNEL_SM100, _dt(v))
+    desc = _desc_from_codes(q_idx, k_idx, v, d, causal, scale, 0, kernel, _dt(v))
     B, H, n_q, _ = q_idx.shape
     o = torch.empty((B, H, n_q, v.shape[-1]), dtype=v.dtype, device=v.device)
     lse = torch.empty((B, H, n_q), dtype=torch.float32, device=v.device)

@@ -13,6 +13,7 @@ sys.path.insert(0, ROOT)
 from paper_2603_22300_b200 import inputs, sfa  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+kern = {"sm100": sfa.KERNEL_SM100, "pair": sfa.KERNEL_SM100_PAIR}[sys.argv[2] if len(sys.argv) > 2 else "sm100"]
 B, H, H_kv, d, d_v, k = 1, 2, 1, 128, 128, 16
 dev = "cuda"
 Q = sfa.gen_fill(torch.empty((B, H, n, d), dtype=torch.bfloat16, device=dev), 3, inputs.TID_Q)
@@ -21,7 +22,7 @@ V = sfa.gen_fill(torch.empty((B, H_kv, n, d_v), dtype=torch.bfloat16, device=dev
 qi, qv = sfa.topk_codes(Q, k)
 ki, kv = sfa.topk_codes(K, k)
 for _ in range(2):
-    o, lse, S, tlb = sfa.debug_sm100_scores(qi, qv, ki, kv, V, d=d, causal=False)
+    o, lse, S, tlb = sfa.debug_sm100_scores(qi, qv, ki, kv, V, d=d, causal=False, kernel=kern)
 torch.cuda.synchronize()
 raw = tlb.cpu().numpy().view(np.uint64)
 rec = raw[1:]
