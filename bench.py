@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="qwen3", choices=sorted(accounting.CONFIGS))
-    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "sm100", "pair"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "sm100", "pair", "wide"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--k", type=int, default=None, help="override the code size k (sweep)")
@@ -329,7 +329,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     kernel = {"auto": sfa.KERNEL_AUTO, "simt": sfa.KERNEL_SIMT, "sm100": sfa.KERNEL_SM100,
-              "pair": sfa.KERNEL_SM100_PAIR}[args.kernel]
+              "pair": sfa.KERNEL_SM100_PAIR, "wide": sfa.KERNEL_SM100_WIDE}[args.kernel]
     dt = torch.bfloat16 if W.dtype == "bf16" else torch.float32
     seed = accounting.SEEDS[args.config]
     B, H, H_kv, n, d, d_v, k = W.B, W.H, W.H_kv, W.n, W.d, W.d_v, W.k

@@ -60,7 +60,8 @@ typedef enum {
                             support overlaps, FFMA P.V (the only fp32 path: reading A12)             */
     SFA_KERNEL_SM100 = 2, /* sm_100a kernel (bf16 only): key codes decompressed on chip, S = Q~ K~^T and
                             O += P V on tcgen05 tensor cores, S/P/O in TMEM, V by TMA    */
-    SFA_KERNEL_SM100_PAIR = 3 /* the same with M = 256 MMAs over CTA pairs (cta_group::2); bf16, d_v = 128 */
+    SFA_KERNEL_SM100_PAIR = 3, /* the same with M = 256 MMAs over CTA pairs (cta_group::2); bf16, d_v = 128 */
+    SFA_KERNEL_SM100_WIDE = 4  /* the same with 256-key score tiles (N = 256 MMAs), P apart from S in TMEM   */
 } sfa_kernel;
 
 SFA_API const char *sfa_status_string(sfa_status s);

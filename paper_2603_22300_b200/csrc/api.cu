@@ -26,10 +26,11 @@ sfa_status validate_desc(const sfa_attn_desc *d) {
     if (d->causal != 0 && d->causal != 1) return SFA_ERR_INVALID_ARGUMENT;
     if (!(d->scale > 0.f) || !isfinite(d->scale)) return SFA_ERR_INVALID_ARGUMENT;
     if (d->dtype != SFA_F32 && d->dtype != SFA_BF16) return SFA_ERR_INVALID_ARGUMENT;
-    if (d->kernel < SFA_KERNEL_AUTO || d->kernel > SFA_KERNEL_SM100_PAIR) return SFA_ERR_INVALID_ARGUMENT;
+    if (d->kernel < SFA_KERNEL_AUTO || d->kernel > SFA_KERNEL_SM100_WIDE) return SFA_ERR_INVALID_ARGUMENT;
     if (d->d != 64 && d->d != 128) return SFA_ERR_UNSUPPORTED;
     if (d->d_v != 64 && d->d_v != 128) return SFA_ERR_UNSUPPORTED;
-    if ((d->kernel == SFA_KERNEL_SM100 || d->kernel == SFA_KERNEL_SM100_PAIR) && d->dtype != SFA_BF16)
+    if ((d->kernel == SFA_KERNEL_SM100 || d->kernel == SFA_KERNEL_SM100_PAIR || d->kernel == SFA_KERNEL_SM100_WIDE) &&
+        d->dtype != SFA_BF16)
         return SFA_ERR_UNSUPPORTED;
     if (d->kernel == SFA_KERNEL_SM100_PAIR && d->d_v != 128) return SFA_ERR_UNSUPPORTED;
     if ((d->n_kv + 63) / 64 > (int64_t)INT32_MAX) return SFA_ERR_UNSUPPORTED;
@@ -114,6 +115,7 @@ sfa_status run_attn_prepared(const sfa_attn_desc *d, const uint8_t *q_idx, const
                              float *dbg = nullptr) {
     const AttnParams p = make_params(d, q_idx, q_val, k_idx, k_val, v, o, lse, ws);
     if (d->kernel == SFA_KERNEL_SM100_PAIR) return from_launch(launch_attn_sm100_pair(p, d->d, d->d_v, st, dbg));
+    if (d->kernel == SFA_KERNEL_SM100_WIDE) return from_launch(launch_attn_sm100_wide(p, d->d, d->d_v, st, dbg));
     if (!uses_simt(d)) return from_launch(launch_attn_sm100(p, d->d, d->d_v, st, dbg));
     return from_cuda(launch_attn_simt(p, d->dtype == SFA_BF16, d->d, d->d_v, st));
 }

@@ -41,5 +41,7 @@ cudaError_t launch_attn_simt(const AttnParams &p, bool bf16, int d, int d_v, cud
 cudaError_t launch_attn_sm100(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
 // the same forward with M = 256 MMAs over CTA pairs (attn_sm100_pair.cu); d_v = 128 only
 cudaError_t launch_attn_sm100_pair(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
+// the same forward with 256-key score tiles and P apart from S (attn_sm100_wide.cu)
+cudaError_t launch_attn_sm100_wide(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
 
 }  // namespace sfa

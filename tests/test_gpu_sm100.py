@@ -83,8 +83,16 @@ def test_peaked_rows_trigger_rescale(lib):
 # ---------------------------------------------------------------------------------------------
 # M = 256 CTA-pair kernel (attn_sm100_pair.cu): same checks
 # ---------------------------------------------------------------------------------------------
+VARIANTS = ["pair", "wide"]  # SFA_KERNEL_SM100_PAIR / SFA_KERNEL_SM100_WIDE
+
+
+def _kern(lib, name):
+    return {"pair": lib.KERNEL_SM100_PAIR, "wide": lib.KERNEL_SM100_WIDE}[name]
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("d,k", [(128, 16), (64, 8), (128, 128)])
-def test_pair_score_tile_is_exact_overlap_sum(lib, d, k):
+def test_variant_score_tile_is_exact_overlap_sum(lib, variant, d, k):
     import torch
     B, H, H_kv, n, d_v = 1, 2, 1, 128, 128
     q, kx, v = host_qkv(201 + k, B, H, H_kv, n, d, d_v, "bf16")
@@ -92,35 +100,40 @@ def test_pair_score_tile_is_exact_overlap_sum(lib, d, k):
     ki, kv = oracle_codes(kx, k)
     o, lse, S, _ = lib.debug_sm100_scores(to_torch(qi, "u8"), to_torch(qv, "bf16"), to_torch(ki, "u8"),
                                           to_torch(kv, "bf16"), to_torch(v, "bf16"), d=d,
-                                          kernel=lib.KERNEL_SM100_PAIR)
+                                          kernel=_kern(lib, variant))
     torch.cuda.synchronize()
     S = S.cpu().numpy().astype(np.float64)
     ref = dense_from_codes(qi[0, 0], qv[0, 0], d) @ dense_from_codes(ki[0, 0], kv[0, 0], d).T
     np.testing.assert_allclose(S, ref, rtol=1e-6, atol=1e-6 * np.abs(ref).max())
 
 
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("shape", [
     (1, 4, 2, 256, 128, 128, 16),   # GQA: pairs of heads
     (1, 3, 1, 384, 128, 128, 16),   # odd group: pairs of consecutive q blocks, last pair half empty
     (2, 2, 2, 300, 64, 128, 8),     # MHA, d = 64, ragged
     (1, 2, 1, 515, 128, 128, 32),
     (1, 2, 2, 1, 128, 128, 4),      # a single token
+    (1, 2, 2, 700, 64, 64, 8),      # d_v = 64 (wide only)
 ])
 @pytest.mark.parametrize("causal", [True, False])
-def test_pair_against_oracle(lib, shape, causal):
+def test_variant_against_oracle(lib, variant, shape, causal):
     import torch
     B, H, H_kv, n, d, d_v, k = shape
+    if variant == "pair" and d_v != 128:
+        pytest.skip("the pair kernel splits d_v = 128 over the CTA pair")
     q, kx, v = host_qkv(56, B, H, H_kv, n, d, d_v, "bf16")
     qi, qv = oracle_codes(q, k)
     ki, kv = oracle_codes(kx, k)
     o_ref, l_ref = oracle.attn_fwd(qi, qv, ki, kv, v, d=d, causal=causal)
     o, lse = lib.attn_fwd(to_torch(qi, "u8"), to_torch(qv, "bf16"), to_torch(ki, "u8"), to_torch(kv, "bf16"),
-                          to_torch(v, "bf16"), d=d, causal=causal, kernel=lib.KERNEL_SM100_PAIR)
+                          to_torch(v, "bf16"), d=d, causal=causal, kernel=_kern(lib, variant))
     torch.cuda.synchronize()
     assert_attn_close(from_torch(o), from_torch(lse), o_ref, l_ref, "bf16")
 
 
-def test_pair_peaked_rows_and_q_pos0(lib):
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_variant_peaked_rows_and_q_pos0(lib, variant):
     import torch
     B, H, H_kv, n, d, d_v, k = 1, 2, 1, 640, 128, 128, 16
     q, kx, v = host_qkv(8, B, H, H_kv, n, d, d_v, "bf16", variant="lattice")
@@ -129,6 +142,6 @@ def test_pair_peaked_rows_and_q_pos0(lib):
     o_ref, l_ref = oracle.attn_fwd(qi[:, :, 200:], qv[:, :, 200:], ki, kv, v, d=d, scale=0.5, q_pos0=200)
     o, lse = lib.attn_fwd(to_torch(qi[:, :, 200:], "u8"), to_torch(qv[:, :, 200:], "bf16"), to_torch(ki, "u8"),
                           to_torch(kv, "bf16"), to_torch(v, "bf16"), d=d, scale=0.5, q_pos0=200,
-                          kernel=lib.KERNEL_SM100_PAIR)
+                          kernel=_kern(lib, variant))
     torch.cuda.synchronize()
     assert_attn_close(from_torch(o), from_torch(lse), o_ref, l_ref, "bf16")

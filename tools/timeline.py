@@ -13,7 +13,7 @@ sys.path.insert(0, ROOT)
 from paper_2603_22300_b200 import inputs, sfa  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
-kern = {"sm100": sfa.KERNEL_SM100, "pair": sfa.KERNEL_SM100_PAIR}[sys.argv[2] if len(sys.argv) > 2 else "sm100"]
+kern = {"sm100": sfa.KERNEL_SM100, "pair": sfa.KERNEL_SM100_PAIR, "wide": sfa.KERNEL_SM100_WIDE}[sys.argv[2] if len(sys.argv) > 2 else "sm100"]
 B, H, H_kv, d, d_v, k = 1, 2, 1, 128, 128, 16
 dev = "cuda"
 Q = sfa.gen_fill(torch.empty((B, H, n, d), dtype=torch.bfloat16, device=dev), 3, inputs.TID_Q)
