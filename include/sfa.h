@@ -158,6 +158,17 @@ SFA_API sfa_status sfa_forward_host(const sfa_attn_desc *desc, const void *q_hos
                             void *o_host, float *lse_host, void *q_dev, void *k_dev, void *v_dev, void *o_dev,
                             float *lse_dev, void *scratch, size_t scratch_bytes, sfa_stream_t stream);
 
+/* Same as sfa_forward_host, pipelined: the B*H_kv independent (batch, kv head) units -- contiguous in
+ * every tensor -- are split into `chunks` (1..64) groups; group c's host->device copies, its stage 1+2
+ * kernels (on `stream`) and its device->host copies run on three streams, so copies of one group
+ * overlap the kernels of its neighbours.  Host buffers must be pinned for the copies to overlap.
+ * Results are identical to sfa_forward_host (each unit is computed by the same kernels). Creates and
+ * destroys two internal streams and 2*chunks events per call; synchronises before returning. */
+SFA_API sfa_status sfa_forward_host_pipelined(const sfa_attn_desc *desc, const void *q_host, const void *k_host,
+                                              const void *v_host, void *o_host, float *lse_host, void *q_dev,
+                                              void *k_dev, void *v_dev, void *o_dev, float *lse_dev, void *scratch,
+                                              size_t scratch_bytes, int32_t chunks, sfa_stream_t stream);
+
 /* Diagnostic (tests only): runs sfa_attn_fwd with the sm_100a kernel (desc->dtype must be bf16 and
  * desc->kernel not SIMT) and also writes the raw fp32 score tile S = Q~ K~^T (unscaled sums of
  * support overlaps) of the first key tile of work item 0 -- query tile 0, the last

@@ -251,6 +251,20 @@ size_t sfa_forward_scratch_bytes(const sfa_attn_desc *desc) {
     return scratch_layout(desc).total;
 }
 
+// stages 1 + 2 with the non-finite flag OR-ed into `status` (not reset here)
+static sfa_status forward_impl(const sfa_attn_desc *desc, const void *q, const void *k, const void *v, void *o,
+                               float *lse, uint8_t *S, uint32_t *status, cudaStream_t st) {
+    const Scratch L = scratch_layout(desc);
+    const bool bf16 = desc->dtype == SFA_BF16;
+    cudaError_t e = launch_topk(q, bf16, (int64_t)desc->B * desc->H * desc->n_q, desc->d, desc->d, desc->k,
+                                S + L.q_idx, S + L.q_val, status, st);
+    if (e != cudaSuccess) return SFA_ERR_CUDA;
+    e = launch_topk(k, bf16, (int64_t)desc->B * desc->H_kv * desc->n_kv, desc->d, desc->d, desc->k, S + L.k_idx,
+                    S + L.k_val, status, st);
+    if (e != cudaSuccess) return SFA_ERR_CUDA;
+    return run_attn(desc, S + L.q_idx, S + L.q_val, S + L.k_idx, S + L.k_val, v, o, lse, S + L.ws, st);
+}
+
 sfa_status sfa_forward(const sfa_attn_desc *desc, const void *q, const void *k, const void *v, void *o, float *lse,
                        void *scratch, size_t scratch_bytes, sfa_stream_t stream) {
     sfa_status s = validate_desc(desc);
@@ -264,16 +278,8 @@ sfa_status sfa_forward(const sfa_attn_desc *desc, const void *q, const void *k, 
     uint8_t *S = (uint8_t *)scratch;
     cudaStream_t st = (cudaStream_t)stream;
     uint32_t *status = (uint32_t *)(S + L.status);
-    cudaError_t e = cudaMemsetAsync(status, 0, 4, st);
-    if (e != cudaSuccess) return SFA_ERR_CUDA;
-    const bool bf16 = desc->dtype == SFA_BF16;
-    e = launch_topk(q, bf16, (int64_t)desc->B * desc->H * desc->n_q, desc->d, desc->d, desc->k, S + L.q_idx,
-                    S + L.q_val, status, st);
-    if (e != cudaSuccess) return SFA_ERR_CUDA;
-    e = launch_topk(k, bf16, (int64_t)desc->B * desc->H_kv * desc->n_kv, desc->d, desc->d, desc->k, S + L.k_idx,
-                    S + L.k_val, status, st);
-    if (e != cudaSuccess) return SFA_ERR_CUDA;
-    return run_attn(desc, S + L.q_idx, S + L.q_val, S + L.k_idx, S + L.k_val, v, o, lse, S + L.ws, st);
+    if (cudaMemsetAsync(status, 0, 4, st) != cudaSuccess) return SFA_ERR_CUDA;
+    return forward_impl(desc, q, k, v, o, lse, S, status, st);
 }
 
 sfa_status sfa_forward_host(const sfa_attn_desc *desc, const void *q_host, const void *k_host, const void *v_host,
@@ -303,6 +309,98 @@ sfa_status sfa_forward_host(const sfa_attn_desc *desc, const void *q_host, const
     if (cudaMemcpyAsync(&status, (uint8_t *)scratch + L.status, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess)
         return SFA_ERR_CUDA;
     if (cudaStreamSynchronize(st) != cudaSuccess) return SFA_ERR_CUDA;
+    return status ? SFA_ERR_INVALID_INPUT : SFA_OK;
+}
+
+sfa_status sfa_forward_host_pipelined(const sfa_attn_desc *desc, const void *q_host, const void *k_host,
+                                      const void *v_host, void *o_host, float *lse_host, void *q_dev, void *k_dev,
+                                      void *v_dev, void *o_dev, float *lse_dev, void *scratch, size_t scratch_bytes,
+                                      int32_t chunks, sfa_stream_t stream) {
+    sfa_status s = validate_desc(desc);
+    if (s != SFA_OK) return s;
+    if (!q_host || !k_host || !v_host || !o_host || !lse_host) return SFA_ERR_INVALID_ARGUMENT;
+    if (!q_dev || !k_dev || !v_dev || !o_dev || !lse_dev || !scratch || chunks < 1) return SFA_ERR_INVALID_ARGUMENT;
+    if (scratch_bytes < scratch_layout(desc).total) return SFA_ERR_RESOURCE;
+    const int R = desc->H / desc->H_kv;
+    const int64_t units = (int64_t)desc->B * desc->H_kv;  // (b, kv head): independent, contiguous everywhere
+    const int64_t nch = chunks < units ? chunks : units;
+    const size_t es = esize(desc->dtype);
+    // bytes of one unit in each tensor
+    const size_t uq = (size_t)R * desc->n_q * desc->d * es, uk = (size_t)desc->n_kv * desc->d * es;
+    const size_t uv = (size_t)desc->n_kv * desc->d_v * es, uo = (size_t)R * desc->n_q * desc->d_v * es;
+    const size_t ul = (size_t)R * desc->n_q * 4;
+    cudaStream_t st = (cudaStream_t)stream, s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev_in[64], ev_done[64];
+    if (nch > 64) return SFA_ERR_INVALID_ARGUMENT;
+    if (cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking) != cudaSuccess) return SFA_ERR_CUDA;
+    if (cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaStreamDestroy(s_in);
+        return SFA_ERR_CUDA;
+    }
+    int nev = 0;
+    sfa_status res = SFA_OK;
+    for (; nev < nch; ++nev) {
+        if (cudaEventCreateWithFlags(&ev_in[nev], cudaEventDisableTiming) != cudaSuccess) break;
+        if (cudaEventCreateWithFlags(&ev_done[nev], cudaEventDisableTiming) != cudaSuccess) {
+            cudaEventDestroy(ev_in[nev]);
+            break;
+        }
+    }
+    if (nev < nch) res = SFA_ERR_CUDA;
+    // the caller's stream may carry prior work on the device buffers: the copies start after it
+    cudaEvent_t ev_start;
+    if (res == SFA_OK && cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming) == cudaSuccess) {
+        cudaEventRecord(ev_start, st);
+        cudaStreamWaitEvent(s_in, ev_start, 0);
+        cudaEventDestroy(ev_start);
+    }
+    // one status word per chunk (the 256-byte status area holds 64): no host sync inside the pipeline
+    const Scratch L = scratch_layout(desc);
+    uint32_t *status_dev = (uint32_t *)((uint8_t *)scratch + L.status);
+    if (res == SFA_OK && cudaMemsetAsync(status_dev, 0, 256, st) != cudaSuccess) res = SFA_ERR_CUDA;
+    for (int64_t c = 0; c < nch && res == SFA_OK; ++c) {
+        const int64_t u0 = units * c / nch, u1 = units * (c + 1) / nch, nu = u1 - u0;
+        sfa_attn_desc sub = *desc;  // the chunk as its own problem: nu batches of R query heads, 1 kv head
+        sub.B = (int32_t)nu;
+        sub.H = R;
+        sub.H_kv = 1;
+        auto q8 = [](const void *p, size_t off) { return (const uint8_t *)p + off; };
+        auto w8 = [](void *p, size_t off) { return (uint8_t *)p + off; };
+        bool ok = cudaMemcpyAsync(w8(q_dev, u0 * uq), q8(q_host, u0 * uq), nu * uq, cudaMemcpyHostToDevice, s_in) ==
+                  cudaSuccess;
+        ok = ok && cudaMemcpyAsync(w8(k_dev, u0 * uk), q8(k_host, u0 * uk), nu * uk, cudaMemcpyHostToDevice, s_in) ==
+                       cudaSuccess;
+        ok = ok && cudaMemcpyAsync(w8(v_dev, u0 * uv), q8(v_host, u0 * uv), nu * uv, cudaMemcpyHostToDevice, s_in) ==
+                       cudaSuccess;
+        ok = ok && cudaEventRecord(ev_in[c], s_in) == cudaSuccess;
+        ok = ok && cudaStreamWaitEvent(st, ev_in[c], 0) == cudaSuccess;
+        if (!ok) {
+            res = SFA_ERR_CUDA;
+            break;
+        }
+        res = forward_impl(&sub, w8(q_dev, u0 * uq), w8(k_dev, u0 * uk), w8(v_dev, u0 * uv), w8(o_dev, u0 * uo),
+                           (float *)w8(lse_dev, u0 * ul), (uint8_t *)scratch, status_dev + c, st);
+        if (res != SFA_OK) break;
+        ok = cudaEventRecord(ev_done[c], st) == cudaSuccess && cudaStreamWaitEvent(s_out, ev_done[c], 0) == cudaSuccess;
+        ok = ok && cudaMemcpyAsync(w8(o_host, u0 * uo), w8(o_dev, u0 * uo), nu * uo, cudaMemcpyDeviceToHost, s_out) ==
+                       cudaSuccess;
+        ok = ok && cudaMemcpyAsync(w8(lse_host, u0 * ul), w8(lse_dev, u0 * ul), nu * ul, cudaMemcpyDeviceToHost,
+                                   s_out) == cudaSuccess;
+        if (!ok) res = SFA_ERR_CUDA;
+    }
+    uint32_t status_h[64] = {0};
+    if (res == SFA_OK && cudaMemcpyAsync(status_h, status_dev, 256, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        res = SFA_ERR_CUDA;
+    uint32_t status = 0;
+    if (cudaStreamSynchronize(s_out) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) res = SFA_ERR_CUDA;
+    for (int i = 0; i < nev; ++i) {
+        cudaEventDestroy(ev_in[i]);
+        cudaEventDestroy(ev_done[i]);
+    }
+    cudaStreamDestroy(s_in);
+    cudaStreamDestroy(s_out);
+    if (res != SFA_OK) return res;
+    for (int i = 0; i < 64; ++i) status |= status_h[i];
     return status ? SFA_ERR_INVALID_INPUT : SFA_OK;
 }
 

@@ -67,6 +67,7 @@ def lib() -> ctypes.CDLL:
             "sfa_forward_scratch_bytes": ([D], SZ),
             "sfa_forward": ([D, P, P, P, P, P, P, SZ, P], I32),
             "sfa_forward_host": ([D, P, P, P, P, P, P, P, P, P, P, P, SZ, P], I32),
+            "sfa_forward_host_pipelined": ([D, P, P, P, P, P, P, P, P, P, P, P, SZ, I32, P], I32),
             "sfa_device_supported": ([], I32),
             "sfa_debug_sm100_scores": ([D, P, P, P, P, P, P, P, P, SZ, P, P], I32),
             "sfa_gen_fill": ([P, I32, I64, I64, ctypes.c_uint64, I32, I32, I64, I32, I32, P], I32),
@@ -82,7 +83,7 @@ EXPORTS = ("sfa_status_string", "sfa_topk_codes", "sfa_attn_workspace_bytes", "s
            "sfa_attn_fwd_bucketed", "sfa_key_tile", "sfa_forward_scratch_bytes", "sfa_forward",
            "sfa_forward_host", "sfa_device_supported", "sfa_gen_fill", "sfa_debug_sm100_scores",
            "sfa_attn_prepare", "sfa_attn_fwd_prepared", "sfa_dist_unique_id", "sfa_dist_init", "sfa_dist_destroy",
-           "sfa_dist_staging_bytes", "sfa_dist_allgather_kv", "sfa_dist_unpack_zigzag")
+           "sfa_dist_staging_bytes", "sfa_dist_allgather_kv", "sfa_dist_unpack_zigzag", "sfa_forward_host_pipelined")
 
 
 def _check(code: int, where: str):
@@ -232,9 +233,15 @@ def forward(q, k, v, *, k_code, causal=True, scale=None, q_pos0=0, kernel=KERNEL
     return o, lse
 
 
-def forward_host(desc: AttnDesc, q_host, k_host, v_host, o_host, lse_host, dev_bufs, scratch):
-    """End to end from host (pinned) tensors: H2D copies, the hot path, D2H copies, stream sync."""
+def forward_host(desc: AttnDesc, q_host, k_host, v_host, o_host, lse_host, dev_bufs, scratch, chunks=0):
+    """End to end from host (pinned) tensors: H2D copies, the hot path, D2H copies, stream sync.
+    chunks > 0: the pipelined variant (copies of one chunk overlap the kernels of the others)."""
     qd, kd, vd, od, ld = dev_bufs
+    if chunks:
+        _check(lib().sfa_forward_host_pipelined(ctypes.byref(desc), _p(q_host), _p(k_host), _p(v_host), _p(o_host),
+                                                _p(lse_host), _p(qd), _p(kd), _p(vd), _p(od), _p(ld), _p(scratch),
+                                                scratch.numel(), chunks, _stream()), "sfa_forward_host_pipelined")
+        return
     _check(lib().sfa_forward_host(ctypes.byref(desc), _p(q_host), _p(k_host), _p(v_host), _p(o_host),
                                   _p(lse_host), _p(qd), _p(kd), _p(vd), _p(od), _p(ld), _p(scratch),
                                   scratch.numel(), _stream()), "sfa_forward_host")

@@ -153,6 +153,11 @@ def test_forward_composition_and_host(lib):
     bufs = (torch.empty_like(Q), torch.empty_like(K), torch.empty_like(V), torch.empty_like(o), torch.empty_like(lse))
     lib.forward_host(desc, qh, kh, vh, oh, lh, bufs, scratch)
     assert torch.equal(oh, o.cpu()) and torch.equal(lh, lse.cpu())
+    for chunks in (1, 2, 3, 64):  # pipelined variant: identical results (GQA units (b, kv head) = 2 here)
+        oh.zero_()
+        lh.zero_()
+        lib.forward_host(desc, qh, kh, vh, oh, lh, bufs, scratch, chunks=chunks)
+        assert torch.equal(oh, o.cpu()) and torch.equal(lh, lse.cpu()), chunks
     o_ref, l_ref = oracle.attn_fwd(*oracle_codes(q, k), *oracle_codes(kx, k), v, d=d)
     assert_attn_close(from_torch(o), from_torch(lse), o_ref, l_ref, "bf16")
 
@@ -170,6 +175,9 @@ def test_forward_host_nonfinite(lib):
     bufs = tuple(torch.empty(t.shape, device="cuda") for t in (Q, K, V, oh, lh))
     with pytest.raises(lib.SfaError) as e:
         lib.forward_host(desc, Q, K, V, oh, lh, bufs, scratch)
+    assert e.value.code == 2
+    with pytest.raises(lib.SfaError) as e:
+        lib.forward_host(desc, Q, K, V, oh, lh, bufs, scratch, chunks=4)
     assert e.value.code == 2
 
 
