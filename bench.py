@@ -445,11 +445,12 @@ def main():
     pairs = B * H * accounting.causal_pairs(n, n, 0, W.causal)
     mufu_peak = N_SMS * MUFU_EX2_PER_CLK_SM * pk["sm_max_mhz"] * 1e6  # ex2/s
     achieved = pairs / (attn_ms / 1e3)
-    traffic = None
+    traffic = None  # dram__bytes_read + dram__bytes_write per launch of the attention kernel (ncu --set full)
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.config, {}).get(f"attn_{args.kernel}")
+            ent = json.load(open(tp)).get(args.config, {}).get(f"attn_{args.kernel}")
+            traffic = ent["dram_bytes_per_launch"] if ent else None
         except Exception:
             traffic = None
     topk_bytes = W.topk_bytes()
@@ -458,6 +459,8 @@ def main():
                 "achieved": achieved / 1e9, "peak": mufu_peak / 1e9,
                 "unit": "G pairs/s (1 MUFU ex2 per allowed causal pair)",
                 "frac": achieved / mufu_peak, "traffic": traffic,
+                "traffic_unit": "DRAM bytes per launch (ncu --set full capture, profiles/ncu_traffic.json); "
+                                f"algorithmic minimum {W.attn_min_bytes()} B",
                 "peak_source": f"148 SMs x 16 ex2/clk x {pk['sm_max_mhz']:.0f} MHz (DESIGN.md 'Rooflines')",
                 "other_floors": {
                     # tensor pipe: S = Q~K~^T (2d) + P.V (2 d_v) FLOPs per allowed pair, vs the measured bf16 peak
