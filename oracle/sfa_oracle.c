@@ -36,7 +36,7 @@
  *                    structural intersections ("Efficiency analysis"),
  *                    counted pair by pair.
  *
- * Pins (tests/test_oracle_pins.py, run with -m "not gpu") tie every function above to
+ * Pins (tests/test_oracle_topk.py, tests/test_oracle_attn.py, tests/test_accounting.py; -m "not gpu") tie every function above to
  * something other than itself: brute-force subset enumeration and the SPEC vectors for
  * top-k; torch's fp64 scaled_dot_product_attention at k = d; closed forms (n = 1,
  * disjoint supports, Q = K = V = I); causality perturbation; row sums of P; the hand

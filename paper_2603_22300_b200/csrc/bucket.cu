@@ -56,7 +56,10 @@ __global__ void __launch_bounds__(128) bucket_keys_kernel(const uint8_t *__restr
         cur[lane * FPL + i] = base + loc[i];
         off[lane * FPL + i] = (uint16_t)(base + loc[i]);
     }
-    if (lane == 31) off[D] = (uint16_t)incl;
+    if (lane == 31) {
+        off[D] = (uint16_t)incl;
+        for (int x = D + 1; x < L.off_bytes / 2; ++x) off[x] = 0;  // alignment padding (copied as 16-byte vectors)
+    }
     __syncwarp();
 
     // deterministic stable placement
