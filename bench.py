@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--k", type=int, default=None, help="override the code size k (sweep)")
+    ap.add_argument("--mode", default="forward", choices=["forward", "decode"],
+                    help="decode: SURVEY 8(f) N2, one new query row per sequence over a cached K/V of the config's n")
+    ap.add_argument("--decode-batch", type=int, default=8, help="sequences per GPU in --mode decode")
     ap.add_argument("--shard-seq", action="store_true",
                     help="query-block sharding of one sequence (default for --config long under torchrun, N>1; "
                          "with N=1 it exercises the same NCCL path on one GPU)")
@@ -189,6 +192,84 @@ L2_FLUSH_MB = 512
 
 
 # --------------------------------------------------------------------------------------------
+def run_decode(args, W, rank, world, local):
+    """a decode step -- one query row per (sequence, head) against a K/V cache of n
+    tokens already coded (k-sparse key codes + bf16 V in HBM).  HBM-bound: the algorithmic traffic is
+    the cache read, n * (3k + 2 d_v) bytes per (sequence, kv head)."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_22300_b200 import inputs, sfa
+    dev = torch.device("cuda", local)
+    B, H, H_kv, n, d, d_v, k = args.decode_batch, W.H, W.H_kv, W.n, W.d, W.d_v, W.k
+    seed = accounting.SEEDS[args.config]
+    bf = torch.bfloat16
+    Qn = sfa.gen_fill(torch.empty((B, H, 1, d), dtype=bf, device=dev), seed, inputs.TID_Q, offset=rank * B * H * d)
+    K = sfa.gen_fill(torch.empty((B, H_kv, n, d), dtype=bf, device=dev), seed, inputs.TID_K, offset=rank * B * H_kv * n * d)
+    V = sfa.gen_fill(torch.empty((B, H_kv, n, d_v), dtype=bf, device=dev), seed, inputs.TID_V,
+                     offset=rank * B * H_kv * n * d_v)
+    qi, qv = sfa.topk_codes(Qn, k)
+    ki, kv = sfa.topk_codes(K, k)  # the cache, coded once (not part of a decode step)
+    del K
+    desc = sfa.make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k, d_v=d_v, n_q=1, n_kv=n, q_pos0=n - 1,
+                         kernel=sfa.KERNEL_DECODE)
+    ws = torch.empty(max(sfa.workspace_bytes(desc), 16), dtype=torch.uint8, device=dev)
+    O = torch.empty((B, H, 1, d_v), dtype=bf, device=dev)
+    LSE = torch.empty((B, H, 1), dtype=torch.float32, device=dev)
+    flush = torch.empty(L2_FLUSH_MB * 2 ** 20, dtype=torch.uint8, device=dev)
+    L = sfa.lib()
+    P_ = lambda t: ctypes.c_void_p(t.data_ptr())
+    st = lambda: ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def step():
+        r = L.sfa_attn_fwd_prepared(ctypes.byref(desc), P_(qi), P_(qv), P_(ki), P_(kv), P_(V), P_(O), P_(LSE), P_(ws),
+                                    ws.numel(), st())
+        if r:
+            raise RuntimeError(f"sfa_attn_fwd_prepared failed: {r}")
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for e0, e1 in evs:
+            flush.zero_()
+            e0.record()
+            step()
+            e1.record()
+        torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    cache_bytes = B * H_kv * n * (k * 3 + d_v * 2)
+    io_bytes = B * H * (k * 3 + d_v * 2 + 4)
+    pk = peaks()
+    gbs = (cache_bytes + io_bytes) / (ms / 1e3) / 1e9
+    if rank == 0:
+        line = {"metric": "FlashSFA decode step: tokens/s and HBM GB/s over a k-sparse KV cache (SURVEY 8(f) N2)",
+                "value": B * world / (ms / 1e3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded generator; cache coded with sfa_topk_codes)",
+                "config": {"workload": f"decode: {B} sequences x H={H} (H_kv={H_kv}) x 1 new token over a {n}-token cache, "
+                                       f"d={d}, d_v={d_v}, k={k}", "global_batch": B * world, "seq_len": n,
+                           "parallelism": "weak: independent sequences per rank",
+                           "l2": f"explicit {L2_FLUSH_MB} MB write between steps; cache {cache_bytes / 2**20:.0f} MiB"},
+                "roofline": {"bound": "hbm", "kernel": "decode_partial_kernel + decode_combine_kernel",
+                             "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
+                             "traffic": None, "algorithmic_bytes_per_step": cache_bytes + io_bytes,
+                             "dense_kv_cache_bytes_for_comparison": B * H_kv * n * (d + d_v) * 2},
+                "cpu_baseline": None, "e2e": None, "gpu_launches": 2 * args.steps, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+
+
 def run_sharded(args, W, rank, world, local):
     """Long-context query-block sharding: one sequence of n tokens over `world`
     GPUs, zig-zag chunks, one NCCL all-gather of key codes + V per step (strong scaling)."""
@@ -318,6 +399,13 @@ def main():
 
     from paper_2603_22300_b200 import inputs, sfa
     torch.cuda.set_device(local)
+    if args.mode == "decode":
+        if world > 1 and not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        run_decode(args, W, rank, world, local)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     if args.shard_seq or (args.config == "long" and world > 1):
         if not dist.is_initialized():
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")

@@ -26,13 +26,16 @@ sfa_status validate_desc(const sfa_attn_desc *d) {
     if (d->causal != 0 && d->causal != 1) return SFA_ERR_INVALID_ARGUMENT;
     if (!(d->scale > 0.f) || !isfinite(d->scale)) return SFA_ERR_INVALID_ARGUMENT;
     if (d->dtype != SFA_F32 && d->dtype != SFA_BF16) return SFA_ERR_INVALID_ARGUMENT;
-    if (d->kernel < SFA_KERNEL_AUTO || d->kernel > SFA_KERNEL_SM100_WIDE) return SFA_ERR_INVALID_ARGUMENT;
+    if (d->kernel < SFA_KERNEL_AUTO || d->kernel > SFA_KERNEL_DECODE) return SFA_ERR_INVALID_ARGUMENT;
     if (d->d != 64 && d->d != 128) return SFA_ERR_UNSUPPORTED;
     if (d->d_v != 64 && d->d_v != 128) return SFA_ERR_UNSUPPORTED;
     if ((d->kernel == SFA_KERNEL_SM100 || d->kernel == SFA_KERNEL_SM100_PAIR || d->kernel == SFA_KERNEL_SM100_WIDE) &&
         d->dtype != SFA_BF16)
         return SFA_ERR_UNSUPPORTED;
     if (d->kernel == SFA_KERNEL_SM100_PAIR && d->d_v != 128) return SFA_ERR_UNSUPPORTED;
+    if (d->kernel == SFA_KERNEL_DECODE &&
+        (d->dtype != SFA_BF16 || (int64_t)(d->H / d->H_kv) * d->n_q > 16))
+        return SFA_ERR_UNSUPPORTED;
     if ((d->n_kv + 63) / 64 > (int64_t)INT32_MAX) return SFA_ERR_UNSUPPORTED;
     return SFA_OK;
 }
@@ -41,9 +44,15 @@ BucketLayout layout_of(const sfa_attn_desc *d) {
     return make_layout(d->d, d->k, d->n_kv, key_tile(d->k), d->dtype == SFA_BF16);
 }
 
-// Which attention kernel a desc runs: the sm_100a tensor-core kernel for bf16 unless the caller
-// asks for the CUDA-core kernel, which is also the only fp32 kernel (reading A12).
-bool uses_simt(const sfa_attn_desc *d) { return d->kernel == SFA_KERNEL_SIMT || d->dtype == SFA_F32; }
+// Which attention kernel a desc runs.  AUTO: the CUDA-core kernel for fp32 (reading A12); for bf16
+// the split-KV decode kernel when a kv head has at most 16 query rows (n_q * H / H_kv), else the
+// sm_100a tensor-core kernel.
+int resolve_kernel(const sfa_attn_desc *d) {
+    if (d->kernel == SFA_KERNEL_SIMT || d->dtype == SFA_F32) return SFA_KERNEL_SIMT;
+    if (d->kernel != SFA_KERNEL_AUTO) return d->kernel;
+    return (int64_t)(d->H / d->H_kv) * d->n_q <= 16 ? SFA_KERNEL_DECODE : SFA_KERNEL_SM100;
+}
+bool uses_simt(const sfa_attn_desc *d) { return resolve_kernel(d) == SFA_KERNEL_SIMT; }
 
 size_t bucket_bytes(const sfa_attn_desc *d) {
     const BucketLayout L = layout_of(d);
@@ -56,7 +65,12 @@ size_t vprep_amax_bytes(const sfa_attn_desc *d) { return align_up((int64_t)d->B 
 size_t vprep_bytes(const sfa_attn_desc *d) {
     return vprep_amax_bytes(d) + (size_t)d->B * d->H_kv * d->n_kv * d->d_v * 2;
 }
-size_t ws_bytes(const sfa_attn_desc *d) { return uses_simt(d) ? bucket_bytes(d) : vprep_bytes(d); }
+size_t ws_bytes(const sfa_attn_desc *d) {
+    const int kern = resolve_kernel(d);
+    if (kern == SFA_KERNEL_SIMT) return bucket_bytes(d);
+    if (kern == SFA_KERNEL_DECODE) return decode_workspace_bytes((int64_t)d->B * d->H_kv, d->n_kv, d->d_v);
+    return vprep_bytes(d);
+}
 
 size_t esize(sfa_dtype t) { return t == SFA_BF16 ? 2 : 4; }
 
@@ -103,6 +117,7 @@ sfa_status from_launch(cudaError_t e) {
 sfa_status run_prepare(const sfa_attn_desc *d, const uint8_t *k_idx, const void *k_val, const void *v, void *ws,
                        cudaStream_t st) {
     const AttnParams p = make_params(d, nullptr, nullptr, k_idx, k_val, v, nullptr, nullptr, ws);
+    if (resolve_kernel(d) == SFA_KERNEL_DECODE) return SFA_OK;  // reads the codes and bf16 V as they are
     if (uses_simt(d))
         return from_cuda(launch_bucket(k_idx, k_val, d->dtype == SFA_BF16, d->d, d->k, (int64_t)d->B * d->H_kv,
                                        d->n_kv, p.L, ws, st));
@@ -114,6 +129,8 @@ sfa_status run_attn_prepared(const sfa_attn_desc *d, const uint8_t *q_idx, const
                              const void *k_val, const void *v, void *o, float *lse, void *ws, cudaStream_t st,
                              float *dbg = nullptr) {
     const AttnParams p = make_params(d, q_idx, q_val, k_idx, k_val, v, o, lse, ws);
+    const int kern = resolve_kernel(d);
+    if (kern == SFA_KERNEL_DECODE) return from_launch(launch_decode(p, d->d, d->d_v, st, ws));
     if (d->kernel == SFA_KERNEL_SM100_PAIR) return from_launch(launch_attn_sm100_pair(p, d->d, d->d_v, st, dbg));
     if (d->kernel == SFA_KERNEL_SM100_WIDE) return from_launch(launch_attn_sm100_wide(p, d->d, d->d_v, st, dbg));
     if (!uses_simt(d)) return from_launch(launch_attn_sm100(p, d->d, d->d_v, st, dbg));
@@ -237,7 +254,8 @@ sfa_status sfa_debug_sm100_scores(const sfa_attn_desc *desc, const uint8_t *q_id
                                   void *workspace, size_t workspace_bytes, float *scores, sfa_stream_t stream) {
     sfa_status s = validate_desc(desc);
     if (s != SFA_OK) return s;
-    if (uses_simt(desc)) return SFA_ERR_UNSUPPORTED;
+    const int kern = resolve_kernel(desc);
+    if (kern == SFA_KERNEL_SIMT || kern == SFA_KERNEL_DECODE) return SFA_ERR_UNSUPPORTED;
     if (!q_idx || !q_val || !k_idx || !k_val || !v || !o || !lse || !scores || !workspace) return SFA_ERR_INVALID_ARGUMENT;
     if (workspace_bytes < ws_bytes(desc)) return SFA_ERR_RESOURCE;
     cudaStream_t st = (cudaStream_t)stream;

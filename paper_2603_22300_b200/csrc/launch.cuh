@@ -34,6 +34,10 @@ __device__ __forceinline__ int vprep_head_exp(uint32_t amax_bits) {
     const int E = (int)((amax_bits >> 23) & 0xFF) - 127;
     return E > 14 ? E - 14 : 0;
 }
+// decode shape (rows = n_q * H / H_kv <= 16 per kv head): split-KV CUDA-core kernel + LSE merge
+// (decode.cu); ws >= decode_workspace_bytes
+cudaError_t launch_decode(const AttnParams &p, int d, int d_v, cudaStream_t st, void *ws);
+size_t decode_workspace_bytes(int64_t bh_kv, int64_t n_kv, int d_v);
 cudaError_t launch_attn_simt(const AttnParams &p, bool bf16, int d, int d_v, cudaStream_t stream);
 // sm_100a tcgen05 kernel (bf16); returns cudaErrorNotSupported for shapes it does not cover.
 // dbg (tests only, may be null): receives the raw 128x128 fp32 score tile S = Q~ K~^T of the
