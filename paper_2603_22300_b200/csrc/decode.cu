@@ -9,14 +9,17 @@
 //
 // Split-KV: CTA (b, kv head g, split s) owns keys [s*chunk, (s+1)*chunk).  The group's query rows
 // (R = H/H_kv heads x n_q rows) are decompressed into shared memory as fp32 (q~ scaled by
-// scale*log2 e).  Each warp walks 32-key blocks: lane l scores key l of the block against every row
-// with k FMAs (its code read with 16-byte loads), the warp reduces the block max per row, updates
-// the running max (online softmax, fp32), then accumulates O[row][:] += p V[key] with lanes over
-// d_v (V rows read coalesced, 8 bytes per lane) and p broadcast by shuffles.  Each warp keeps its
-// own (m, l, O) in registers; the CTA merges its warps in shared memory and writes one partial per
-// split; `decode_combine_kernel` merges the splits with their log-sum-exps.  fp32 throughout, bf16
-// V read as is; O rounded to bf16 once.
+// scale*log2 e).  A producer warp streams the split's V rows through a 3-stage shared-memory ring
+// of 256-key blocks with cp.async.bulk (mbarrier transaction counts), so ~130 KB of V is in flight
+// per SM; 8 consumer warps take 32 keys of every block each: lane l scores its key against every
+// row with k FMAs from the key's code (16-byte loads prefetched one block ahead), the warp reduces
+// the block max per row and updates the running max (online softmax, fp32), then accumulates
+// O[row][:] += p V[key] from the ring with lanes over d_v and p broadcast by shuffles.  Each warp
+// keeps its own (m, l, O) in registers; the CTA merges its warps (in the drained ring) and writes
+// one partial per split; `decode_combine_kernel` merges the splits with their log-sum-exps.  fp32
+// throughout, bf16 V read as is; O rounded to bf16 once.
 #include "launch.cuh"
+#include "sm100.cuh"
 
 namespace sfa {
 
@@ -44,33 +47,68 @@ struct DecArgs {
     int64_t chunk;
 };
 
-template <int DV, int ROWS>
-__global__ void __launch_bounds__(DEC_THREADS) decode_partial_kernel(const DecArgs a) {
-    constexpr int DPL = DV / 32;  // value dims per lane (2 or 4)
-    extern __shared__ __align__(16) float dsm[];
-    float *qs = dsm;                                         // [ROWS][d] fp32 decompressed, pre-scaled queries
-    float(*red_m)[ROWS] = reinterpret_cast<float(*)[ROWS]>(dsm + ROWS * a.d);  // [warps][ROWS]
-    float(*red_l)[ROWS] = red_m + DEC_WARPS;
-    float(*red_o)[ROWS][DV] = reinterpret_cast<float(*)[ROWS][DV]>(dsm + ROWS * a.d + 2 * DEC_WARPS * ROWS);
+constexpr int DB = 256;  // keys per V block streamed by the producer
+constexpr int NST = 3;   // V ring stages
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+// one key's code in registers (k % 8 == 0, k <= 32), loaded a block ahead of its use
+struct Code32 {
+    uint2 idx[4];
+    uint4 val[4];
+};
+
+// CW consumer warps (8 or 16): warps 8g..8g+7 take the blocks blk = g (mod CW / 8), 32 keys each
+template <int DV, int ROWS, int CW>
+__global__ void __launch_bounds__(CW * 32 + 32, 1) decode_partial_kernel(const DecArgs a) {
+    constexpr int DPL = DV / 32;      // value dims per lane (2 or 4)
+    constexpr int VT = DB * DV * 2;   // bytes of one V block
+    extern __shared__ __align__(1024) uint8_t dsm_raw[];
+    float *qs = reinterpret_cast<float *>(dsm_raw);                        // [d][ROWS] pre-scaled queries
+    float *pbuf = reinterpret_cast<float *>(dsm_raw + ROWS * a.d * 4);     // [CW][32][ROWS] weights
+    uint8_t *vring = dsm_raw + ((ROWS * a.d * 4 + CW * 32 * ROWS * 4 + 1023) & ~1023);  // [NST][DB][DV] bf16
+    uint64_t *bars = reinterpret_cast<uint64_t *>(vring + NST * VT);        // full[NST], empty[NST]
+    const uint32_t vring_s = (uint32_t)__cvta_generic_to_shared(vring);
+    const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
     const int bg = blockIdx.x, split = blockIdx.y;
     const int b = bg / a.H_kv, g = bg % a.H_kv;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rows = a.R * (int)a.n_q;
-    // decompress the group's query rows: row = hr * n_q + i (hr = head within the group)
-    for (int x = threadIdx.x; x < ROWS * a.d; x += DEC_THREADS) qs[x] = 0.f;
-    __syncthreads();
-    for (int row = threadIdx.x; row < rows; row += DEC_THREADS) {
-        const int hr = row / (int)a.n_q, i = row % (int)a.n_q;
-        const int64_t qrow = ((int64_t)b * a.H + g * a.R + hr) * a.n_q + i;
-        for (int t = 0; t < a.k; ++t)
-            qs[row * a.d + a.q_idx[qrow * a.k + t]] = __uint_as_float((uint32_t)a.q_val[qrow * a.k + t] << 16) * a.c_scale;
-    }
-    __syncthreads();
-
     const int64_t k0 = (int64_t)split * a.chunk;
     int64_t k1 = k0 + a.chunk;
     if (k1 > a.n_kv) k1 = a.n_kv;
+    const int nblk = k1 > k0 ? (int)((k1 - k0 + DB - 1) / DB) : 0;
     const int64_t kvbase = ((int64_t)b * a.H_kv + g) * a.n_kv;
+
+    for (int x = threadIdx.x; x < ROWS * a.d; x += blockDim.x) qs[x] = 0.f;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NST; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s + 8 * i));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_s + 8 * (NST + i)), "r"(DEC_WARPS));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    for (int row = threadIdx.x; row < rows; row += blockDim.x) {
+        const int hr = row / (int)a.n_q, i = row % (int)a.n_q;
+        const int64_t qrow = ((int64_t)b * a.H + g * a.R + hr) * a.n_q + i;
+        for (int t = 0; t < a.k; ++t)
+            qs[a.q_idx[qrow * a.k + t] * ROWS + row] = __uint_as_float((uint32_t)a.q_val[qrow * a.k + t] << 16) * a.c_scale;
+    }
+    __syncthreads();
+
+    auto wait = [](uint32_t bar, uint32_t parity) {
+        asm volatile(
+            "{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n\t}" ::"r"(
+                bar),
+            "r"(parity)
+            : "memory");
+    };
+
     float m[ROWS], l[ROWS], acc[ROWS][DPL];
 #pragma unroll
     for (int r = 0; r < ROWS; ++r) {
@@ -79,108 +117,176 @@ __global__ void __launch_bounds__(DEC_THREADS) decode_partial_kernel(const DecAr
 #pragma unroll
         for (int e = 0; e < DPL; ++e) acc[r][e] = 0.f;
     }
-    // warps take interleaved 32-key blocks of the split
-    for (int64_t kb = k0 + (int64_t)warp * 32; kb < k1; kb += (int64_t)DEC_WARPS * 32) {
-        const int64_t key = kb + lane;
-        const bool kval = key < k1;
-        // ---- step 4: scores of key `key` against every row from its code
-        float s[ROWS];
+    constexpr int GROUPS = CW / DEC_WARPS;
+    if (warp == CW) {
+        // ============ producer: V blocks of the split into the ring (cp.async.bulk, mbarrier tx) ============
+        if (lane == 0) {
+            for (int blk = 0; blk < nblk; ++blk) {
+                const int st = blk % NST, u = blk / NST;
+                wait(bar_s + 8 * (NST + st), (u & 1) ^ 1);
+                const int64_t ks = k0 + (int64_t)blk * DB;
+                const int nk = (int)((k1 - ks) < DB ? (k1 - ks) : DB);
+                const uint32_t bytes = (uint32_t)nk * DV * 2;
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s + 8 * st), "r"(bytes)
+                             : "memory");
+                bulk_g2s(vring_s + st * VT, a.v + (kvbase + ks) * DV, bytes, bar_s + 8 * st);
+            }
+        }
+    } else {
+        // ============ consumers: warp w takes keys [32 (w % 8), +32) of blocks w / 8, w / 8 + GROUPS, ... ============
+        const int sub = warp % DEC_WARPS, grp0 = warp / DEC_WARPS;
+        const bool pre = (a.k & 7) == 0 && a.k <= 32;
+        Code32 nxt;
+        auto load_code = [&](Code32 &c, int64_t key) {
+            const uint2 *ci = reinterpret_cast<const uint2 *>(a.k_idx + (kvbase + key) * a.k);
+            const uint4 *cv = reinterpret_cast<const uint4 *>(a.k_val + (kvbase + key) * a.k);
 #pragma unroll
-        for (int r = 0; r < ROWS; ++r) s[r] = 0.f;
-        if (kval) {
-            const uint8_t *ci = a.k_idx + (kvbase + key) * a.k;
-            const uint16_t *cv = a.k_val + (kvbase + key) * a.k;
-            if ((a.k & 7) == 0) {  // 8 codes per step: 8-byte index + 16-byte value loads
-                for (int t0 = 0; t0 < a.k; t0 += 8) {
-                    const uint2 ii = __ldg(reinterpret_cast<const uint2 *>(ci + t0));
-                    const uint4 vv = __ldg(reinterpret_cast<const uint4 *>(cv + t0));
-                    const uint32_t iw[2] = {ii.x, ii.y}, vw[4] = {vv.x, vv.y, vv.z, vv.w};
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const int f = (iw[e >> 2] >> (8 * (e & 3))) & 0xFF;
-                        const float kvf = __uint_as_float((e & 1) ? (vw[e >> 1] & 0xFFFF0000u) : (vw[e >> 1] << 16));
-#pragma unroll
-                        for (int r = 0; r < ROWS; ++r) s[r] = fmaf(qs[r * a.d + f], kvf, s[r]);
-                    }
+            for (int gg = 0; gg < 4; ++gg)
+                if (8 * gg < a.k) {
+                    c.idx[gg] = __ldg(ci + gg);
+                    c.val[gg] = __ldg(cv + gg);
                 }
-            } else {
+        };
+        {
+            const int64_t key = k0 + (int64_t)grp0 * DB + sub * 32 + lane;
+            if (pre && grp0 < nblk && key < k1) load_code(nxt, key);
+        }
+        for (int blk = grp0; blk < nblk; blk += GROUPS) {
+            const int st = blk % NST, u = blk / NST;
+            const int64_t kb = k0 + (int64_t)blk * DB + sub * 32;
+            const int64_t key = kb + lane;
+            const bool kval = key < k1;
+            // ---- step 4: scores from the key's code (prefetched one block ahead)
+            float sc[ROWS];
+#pragma unroll
+            for (int r = 0; r < ROWS; ++r) sc[r] = 0.f;
+            if (pre) {
+                const Code32 cur = nxt;
+                const int64_t nkey = key + (int64_t)GROUPS * DB;
+                if (blk + GROUPS < nblk && nkey < k1) load_code(nxt, nkey);
+                if (kval) {
+#pragma unroll
+                    for (int gg = 0; gg < 4; ++gg)
+                        if (8 * gg < a.k) {
+                            const uint32_t iw[2] = {cur.idx[gg].x, cur.idx[gg].y};
+                            const uint32_t vw[4] = {cur.val[gg].x, cur.val[gg].y, cur.val[gg].z, cur.val[gg].w};
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                const int f = (iw[e >> 2] >> (8 * (e & 3))) & 0xFF;
+                                const float kvf =
+                                    __uint_as_float((e & 1) ? (vw[e >> 1] & 0xFFFF0000u) : (vw[e >> 1] << 16));
+                                const float4 *qf = reinterpret_cast<const float4 *>(qs + f * ROWS);
+#pragma unroll
+                                for (int r4 = 0; r4 < ROWS / 4; ++r4) {
+                                    const float4 qq = qf[r4];
+                                    sm100::ffma2v(sc[4 * r4], sc[4 * r4 + 1], qq.x, qq.y, kvf, kvf, sc[4 * r4], sc[4 * r4 + 1]);
+                                    sm100::ffma2v(sc[4 * r4 + 2], sc[4 * r4 + 3], qq.z, qq.w, kvf, kvf, sc[4 * r4 + 2],
+                                                  sc[4 * r4 + 3]);
+                                }
+                            }
+                        }
+                }
+            } else if (kval) {
+                const uint8_t *ci = a.k_idx + (kvbase + key) * a.k;
+                const uint16_t *cv = a.k_val + (kvbase + key) * a.k;
                 for (int t = 0; t < a.k; ++t) {
                     const int f = __ldg(ci + t);
                     const float kvf = __uint_as_float((uint32_t)__ldg(cv + t) << 16);
 #pragma unroll
-                    for (int r = 0; r < ROWS; ++r) s[r] = fmaf(qs[r * a.d + f], kvf, s[r]);
+                    for (int r = 0; r < ROWS; ++r) sc[r] = fmaf(qs[f * ROWS + r], kvf, sc[r]);
                 }
             }
-        }
-        // ---- step 5: causal / ragged mask; step 6: online softmax per row (warp-wide block max)
-        float p[ROWS];
-#pragma unroll
-        for (int r = 0; r < ROWS; ++r) {
-            bool ok = kval && r < rows;
-            if (ok && a.causal) ok = key <= a.q_pos0 + (r % (int)a.n_q);
-            float x = ok ? s[r] : -INFINITY;
-            float bm = x;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
-            const float mn = fmaxf(m[r], bm);
-            const float ms = mn == -INFINITY ? 0.f : mn;
-            const float alpha = fast_exp2(m[r] - ms);  // m = -inf -> 0
-            p[r] = ok ? fast_exp2(x - ms) : 0.f;
-            float ps = p[r];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
-            l[r] = l[r] * alpha + ps;
-#pragma unroll
-            for (int e = 0; e < DPL; ++e) acc[r][e] *= alpha;
-            m[r] = mn;
-        }
-        // ---- step 7: O[r][lane dims] += sum over the block's keys of p * V[key][lane dims]
-        const int nk = (int)((k1 - kb) < 32 ? (k1 - kb) : 32);
-        const uint16_t *vb = a.v + (kvbase + kb) * DV + lane * DPL;
-#pragma unroll 4
-        for (int kk = 0; kk < nk; ++kk) {
-            float vv[DPL];
-            if (DPL == 4) {
-                const uint2 w = __ldg(reinterpret_cast<const uint2 *>(vb + (int64_t)kk * DV));
-                vv[0] = __uint_as_float(w.x << 16);
-                vv[1] = __uint_as_float(w.x & 0xFFFF0000u);
-                vv[2 % DPL] = __uint_as_float(w.y << 16);
-                vv[3 % DPL] = __uint_as_float(w.y & 0xFFFF0000u);
-            } else {
-                const uint32_t w = __ldg(reinterpret_cast<const uint32_t *>(vb + (int64_t)kk * DV));
-                vv[0] = __uint_as_float(w << 16);
-                vv[1 % DPL] = __uint_as_float(w & 0xFFFF0000u);
-            }
+            // ---- steps 5-6: mask + online softmax per row (warp-wide block max and sum)
+            float p[ROWS];
 #pragma unroll
             for (int r = 0; r < ROWS; ++r) {
-                const float pr = __shfl_sync(0xffffffffu, p[r], kk);
+                bool ok = kval && r < rows;
+                if (ok && a.causal) ok = key <= a.q_pos0 + (r % (int)a.n_q);
+                const float x = ok ? sc[r] : -INFINITY;
+                float bm = x;
 #pragma unroll
-                for (int e = 0; e < DPL; ++e) acc[r][e] = fmaf(pr, vv[e], acc[r][e]);
+                for (int o = 16; o > 0; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+                const float mn = fmaxf(m[r], bm);
+                const float ms = mn == -INFINITY ? 0.f : mn;
+                const float alpha = fast_exp2(m[r] - ms);
+                p[r] = ok ? fast_exp2(x - ms) : 0.f;
+                float ps = p[r];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+                l[r] = l[r] * alpha + ps;
+#pragma unroll
+                for (int e = 0; e < DPL; ++e) acc[r][e] *= alpha;
+                m[r] = mn;
             }
+            // ---- step 7: O += p V over this warp's 32 keys, V from the ring, p from shared memory
+            float *pw = pbuf + warp * 32 * ROWS;
+#pragma unroll
+            for (int r4 = 0; r4 < ROWS / 4; ++r4)
+                reinterpret_cast<float4 *>(pw + lane * ROWS)[r4] = make_float4(p[4 * r4], p[4 * r4 + 1], p[4 * r4 + 2], p[4 * r4 + 3]);
+            __syncwarp();
+            wait(bar_s + 8 * st, u & 1);
+            int nk = (int)(k1 - kb);
+            nk = nk < 0 ? 0 : (nk > 32 ? 32 : nk);
+            const uint8_t *vrow = vring + st * VT + (size_t)(sub * 32) * DV * 2 + lane * DPL * 2;
+#pragma unroll 8
+            for (int kk = 0; kk < nk; ++kk) {
+                float vv[4];
+                if (DPL == 4) {
+                    const uint2 w = *reinterpret_cast<const uint2 *>(vrow + (size_t)kk * DV * 2);
+                    vv[0] = __uint_as_float(w.x << 16);
+                    vv[1] = __uint_as_float(w.x & 0xFFFF0000u);
+                    vv[2] = __uint_as_float(w.y << 16);
+                    vv[3] = __uint_as_float(w.y & 0xFFFF0000u);
+                } else {
+                    const uint32_t w = *reinterpret_cast<const uint32_t *>(vrow + (size_t)kk * DV * 2);
+                    vv[0] = __uint_as_float(w << 16);
+                    vv[1] = __uint_as_float(w & 0xFFFF0000u);
+                }
+                const float4 *pk4 = reinterpret_cast<const float4 *>(pw + kk * ROWS);
+#pragma unroll
+                for (int r4 = 0; r4 < ROWS / 4; ++r4) {
+                    const float4 pp = pk4[r4];  // broadcast read
+                    const float pr[4] = {pp.x, pp.y, pp.z, pp.w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int r = 4 * r4 + q;
+#pragma unroll
+                        for (int e = 0; e < DPL; e += 2)
+                            sm100::ffma2v(acc[r][e], acc[r][e + 1], vv[e], vv[e + 1], pr[q], pr[q], acc[r][e], acc[r][e + 1]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_s + 8 * (NST + st)) : "memory");
         }
     }
-    // ---- merge the CTA's warps (shared memory), write this split's partial
+    __syncthreads();  // every V block consumed: the ring is reused for the warps' partials
+    float *red_m = reinterpret_cast<float *>(vring);           // [CW][ROWS]
+    float *red_l = red_m + CW * ROWS;                          // [CW][ROWS]
+    float *red_o = red_l + CW * ROWS;                          // [CW][ROWS][DV]
+    if (warp < CW) {
 #pragma unroll
-    for (int r = 0; r < ROWS; ++r) {
-        if (lane == 0) {
-            red_m[warp][r] = m[r];
-            red_l[warp][r] = l[r];
+        for (int r = 0; r < ROWS; ++r) {
+            if (lane == 0) {
+                red_m[warp * ROWS + r] = m[r];
+                red_l[warp * ROWS + r] = l[r];
+            }
+#pragma unroll
+            for (int e = 0; e < DPL; ++e) red_o[(warp * ROWS + r) * DV + lane * DPL + e] = acc[r][e];
         }
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) red_o[warp][r][lane * DPL + e] = acc[r][e];
     }
     __syncthreads();
     float *part = a.part + ((int64_t)bg * a.nsplit + split) * ROWS * (2 + DV);
-    for (int x = threadIdx.x; x < ROWS * DV; x += DEC_THREADS) {
+    for (int x = threadIdx.x; x < ROWS * DV; x += blockDim.x) {
         const int r = x / DV, c = x % DV;
         float M = -INFINITY;
-        for (int w = 0; w < DEC_WARPS; ++w) M = fmaxf(M, red_m[w][r]);
+        for (int w = 0; w < CW; ++w) M = fmaxf(M, red_m[w * ROWS + r]);
         const float Ms = M == -INFINITY ? 0.f : M;
         float L = 0.f, O = 0.f;
-        for (int w = 0; w < DEC_WARPS; ++w) {
-            const float f = fast_exp2(red_m[w][r] - Ms);
-            L += red_l[w][r] * f;
-            O += red_o[w][r][c] * f;
+        for (int w = 0; w < CW; ++w) {
+            const float f = fast_exp2(red_m[w * ROWS + r] - Ms);
+            L += red_l[w * ROWS + r] * f;
+            O += red_o[(w * ROWS + r) * DV + c] * f;
         }
         part[2 * ROWS + x] = O;
         if (c == 0) {
@@ -216,12 +322,15 @@ __global__ void __launch_bounds__(DV) decode_combine_kernel(const DecArgs a) {
 
 template <int DV, int ROWS>
 cudaError_t launch_decode_t(const DecArgs &a, cudaStream_t st) {
-    const size_t smem = ((size_t)ROWS * a.d + 2 * DEC_WARPS * ROWS + (size_t)DEC_WARPS * ROWS * DV) * 4;
-    auto kern = decode_partial_kernel<DV, ROWS>;
+    constexpr int CW = ROWS <= 4 ? 16 : 8;  // 16 consumer warps when the registers allow
+    const size_t smem = ((size_t)ROWS * a.d * 4 + (size_t)CW * 32 * ROWS * 4 + 1023) / 1024 * 1024 +
+                        (size_t)NST * DB * DV * 2 + 2 * NST * 8 + 1024;
+    static_assert((size_t)CW * ROWS * (2 + DV) * 4 <= (size_t)NST * DB * DV * 2, "merge area fits the V ring");
+    auto kern = decode_partial_kernel<DV, ROWS, CW>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 g1(a.B * a.H_kv, a.nsplit);
-    kern<<<g1, DEC_THREADS, smem, st>>>(a);
+    kern<<<g1, CW * 32 + 32, smem, st>>>(a);
     dim3 g2(a.B * a.H_kv, ROWS);
     decode_combine_kernel<DV, ROWS><<<g2, DV, 0, st>>>(a);
     return cudaGetLastError();
@@ -230,9 +339,9 @@ cudaError_t launch_decode_t(const DecArgs &a, cudaStream_t st) {
 }  // namespace
 
 int decode_nsplit(int64_t bh_kv, int64_t n_kv) {
-    // enough CTAs for ~4 waves over 148 SMs, each split at least 256 keys
-    int64_t want = (148 * 8 + bh_kv - 1) / bh_kv;
-    const int64_t maxs = (n_kv + 255) / 256;
+    // one CTA per SM (the V ring is ~200 KB): about 4 waves over 148 SMs, each split >= 2 V blocks
+    int64_t want = (148 * 4 + bh_kv - 1) / bh_kv;
+    const int64_t maxs = (n_kv + 2 * DB - 1) / (2 * DB);
     if (want > maxs) want = maxs;
     if (want < 1) want = 1;
     if (want > 4096) want = 4096;
@@ -268,7 +377,7 @@ cudaError_t launch_decode(const AttnParams &p, int d, int d_v, cudaStream_t st, 
     a.causal = p.causal;
     a.c_scale = p.scale_log2;
     a.nsplit = decode_nsplit((int64_t)p.B * p.H_kv, p.n_kv);
-    a.chunk = (p.n_kv + a.nsplit - 1) / a.nsplit;
+    a.chunk = ((p.n_kv + a.nsplit - 1) / a.nsplit + DB - 1) / DB * DB;  // whole V blocks per split
     if (rows <= 4) return d_v == 64 ? launch_decode_t<64, 4>(a, st) : launch_decode_t<128, 4>(a, st);
     if (rows <= 8) return d_v == 64 ? launch_decode_t<64, 8>(a, st) : launch_decode_t<128, 8>(a, st);
     return d_v == 64 ? launch_decode_t<64, 16>(a, st) : launch_decode_t<128, 16>(a, st);
