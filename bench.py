@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="qwen3", choices=sorted(accounting.CONFIGS))
-    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "sm100", "pair", "wide"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "sm100", "pair", "wide", "ot"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--k", type=int, default=None, help="override the code size k (sweep)")
@@ -374,7 +374,7 @@ def run_sharded(args, W, rank, world, local):
                            "l2": f"explicit {L2_FLUSH_MB} MB write between timed steps"},
                 "stage_ms": {"topk_qk": stage[0], "allgather_kv": stage[1], "prepare": stage[2], "attn": stage[3]},
                 "allgather_bytes_per_rank": ag_bytes,
-                "roofline": {"bound": "alu", "kernel": "attn_sm100_kernel (steps 4-8), per rank",
+                "roofline": {"bound": "alu", "kernel": ("attn_sm100_ot_kernel" if W.d_v == 128 else "attn_sm100_kernel") + " (steps 4-8), per rank",
                              "achieved": achieved / 1e9, "peak": mufu_peak / 1e9,
                              "unit": "G pairs/s (1 MUFU ex2 per allowed causal pair)", "frac": achieved / mufu_peak,
                              "traffic": None, "peak_source": "148 SMs x 16 ex2/clk x max SM clock"},
@@ -417,7 +417,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     kernel = {"auto": sfa.KERNEL_AUTO, "simt": sfa.KERNEL_SIMT, "sm100": sfa.KERNEL_SM100,
-              "pair": sfa.KERNEL_SM100_PAIR, "wide": sfa.KERNEL_SM100_WIDE}[args.kernel]
+              "pair": sfa.KERNEL_SM100_PAIR, "wide": sfa.KERNEL_SM100_WIDE,
+              "ot": sfa.KERNEL_SM100_OT}[args.kernel]
     dt = torch.bfloat16 if W.dtype == "bf16" else torch.float32
     seed = accounting.SEEDS[args.config]
     B, H, H_kv, n, d, d_v, k = W.B, W.H, W.H_kv, W.n, W.d, W.d_v, W.k
@@ -543,7 +544,10 @@ def main():
             traffic = None
     topk_bytes = W.topk_bytes()
     sm100 = W.dtype == "bf16" and args.kernel != "simt"
-    roofline = {"bound": "alu", "kernel": ("attn_sm100_kernel" if sm100 else "attn_simt_kernel") + " (steps 4-8)",
+    kname = {"auto": "attn_sm100_ot_kernel" if d_v == 128 else "attn_sm100_kernel", "sm100": "attn_sm100_kernel",
+             "ot": "attn_sm100_ot_kernel", "pair": "attn_sm100_pair_kernel", "wide": "attn_sm100_wide_kernel",
+             "simt": "attn_simt_kernel"}[args.kernel if sm100 else "simt"]
+    roofline = {"bound": "alu", "kernel": kname + " (steps 4-8)",
                 "achieved": achieved / 1e9, "peak": mufu_peak / 1e9,
                 "unit": "G pairs/s (1 MUFU ex2 per allowed causal pair)",
                 "frac": achieved / mufu_peak, "traffic": traffic,

@@ -55,16 +55,19 @@ typedef enum { SFA_F32 = 0, SFA_BF16 = 1 } sfa_dtype;
 
 /* Kernel selection for sfa_attn_fwd (desc.kernel). */
 typedef enum {
-    SFA_KERNEL_AUTO = 0, /* SIMT for fp32; for bf16 DECODE when n_q * H / H_kv <= 16, else SM100       */
+    SFA_KERNEL_AUTO = 0, /* SIMT for fp32; for bf16 DECODE when n_q * H / H_kv <= 16, else SM100_OT for
+                            d_v = 128 and SM100 for d_v = 64                                           */
     SFA_KERNEL_SIMT = 1, /* CUDA-core kernel: key-tile feature buckets, shared-memory scatter of the
                             support overlaps, FFMA P.V (the only fp32 path: reading A12)             */
     SFA_KERNEL_SM100 = 2, /* sm_100a kernel (bf16 only): key codes decompressed on chip, S = Q~ K~^T and
                             O += P V on tcgen05 tensor cores, S/P/O in TMEM, V by TMA    */
     SFA_KERNEL_SM100_PAIR = 3, /* the same with M = 256 MMAs over CTA pairs (cta_group::2); bf16, d_v = 128 */
     SFA_KERNEL_SM100_WIDE = 4, /* the same with 256-key score tiles (N = 256 MMAs), P apart from S in TMEM   */
-    SFA_KERNEL_DECODE = 5      /* few query rows over a long cache (n_q * H / H_kv <= 16, bf16): split-KV
+    SFA_KERNEL_DECODE = 5,     /* few query rows over a long cache (n_q * H / H_kv <= 16, bf16): split-KV
                                   CUDA-core kernel reading codes + V, LSE merge.  AUTO picks
                                   it for such shapes.                                                      */
+    SFA_KERNEL_SM100_OT = 6    /* SM100 with a transposed output accumulator: O^T += V^T P^T as N = 256 MMAs
+                                  over both query tiles, P in shared memory (bf16, d_v = 128)              */
 } sfa_kernel;
 
 SFA_API const char *sfa_status_string(sfa_status s);

@@ -26,13 +26,14 @@ sfa_status validate_desc(const sfa_attn_desc *d) {
     if (d->causal != 0 && d->causal != 1) return SFA_ERR_INVALID_ARGUMENT;
     if (!(d->scale > 0.f) || !isfinite(d->scale)) return SFA_ERR_INVALID_ARGUMENT;
     if (d->dtype != SFA_F32 && d->dtype != SFA_BF16) return SFA_ERR_INVALID_ARGUMENT;
-    if (d->kernel < SFA_KERNEL_AUTO || d->kernel > SFA_KERNEL_DECODE) return SFA_ERR_INVALID_ARGUMENT;
+    if (d->kernel < SFA_KERNEL_AUTO || d->kernel > SFA_KERNEL_SM100_OT) return SFA_ERR_INVALID_ARGUMENT;
     if (d->d != 64 && d->d != 128) return SFA_ERR_UNSUPPORTED;
     if (d->d_v != 64 && d->d_v != 128) return SFA_ERR_UNSUPPORTED;
-    if ((d->kernel == SFA_KERNEL_SM100 || d->kernel == SFA_KERNEL_SM100_PAIR || d->kernel == SFA_KERNEL_SM100_WIDE) &&
+    if ((d->kernel == SFA_KERNEL_SM100 || d->kernel == SFA_KERNEL_SM100_PAIR || d->kernel == SFA_KERNEL_SM100_WIDE ||
+         d->kernel == SFA_KERNEL_SM100_OT) &&
         d->dtype != SFA_BF16)
         return SFA_ERR_UNSUPPORTED;
-    if (d->kernel == SFA_KERNEL_SM100_PAIR && d->d_v != 128) return SFA_ERR_UNSUPPORTED;
+    if ((d->kernel == SFA_KERNEL_SM100_PAIR || d->kernel == SFA_KERNEL_SM100_OT) && d->d_v != 128) return SFA_ERR_UNSUPPORTED;
     if (d->kernel == SFA_KERNEL_DECODE &&
         (d->dtype != SFA_BF16 || (int64_t)(d->H / d->H_kv) * d->n_q > 16))
         return SFA_ERR_UNSUPPORTED;
@@ -46,11 +47,12 @@ BucketLayout layout_of(const sfa_attn_desc *d) {
 
 // Which attention kernel a desc runs.  AUTO: the CUDA-core kernel for fp32 (reading A12); for bf16
 // the split-KV decode kernel when a kv head has at most 16 query rows (n_q * H / H_kv), else the
-// sm_100a tensor-core kernel.
+// sm_100a tensor-core kernel: the transposed-output one (SM100_OT) for d_v = 128, SM100 for d_v = 64.
 int resolve_kernel(const sfa_attn_desc *d) {
     if (d->kernel == SFA_KERNEL_SIMT || d->dtype == SFA_F32) return SFA_KERNEL_SIMT;
     if (d->kernel != SFA_KERNEL_AUTO) return d->kernel;
-    return (int64_t)(d->H / d->H_kv) * d->n_q <= 16 ? SFA_KERNEL_DECODE : SFA_KERNEL_SM100;
+    if ((int64_t)(d->H / d->H_kv) * d->n_q <= 16) return SFA_KERNEL_DECODE;
+    return d->d_v == 128 ? SFA_KERNEL_SM100_OT : SFA_KERNEL_SM100;
 }
 bool uses_simt(const sfa_attn_desc *d) { return resolve_kernel(d) == SFA_KERNEL_SIMT; }
 
@@ -131,9 +133,10 @@ sfa_status run_attn_prepared(const sfa_attn_desc *d, const uint8_t *q_idx, const
     const AttnParams p = make_params(d, q_idx, q_val, k_idx, k_val, v, o, lse, ws);
     const int kern = resolve_kernel(d);
     if (kern == SFA_KERNEL_DECODE) return from_launch(launch_decode(p, d->d, d->d_v, st, ws));
-    if (d->kernel == SFA_KERNEL_SM100_PAIR) return from_launch(launch_attn_sm100_pair(p, d->d, d->d_v, st, dbg));
-    if (d->kernel == SFA_KERNEL_SM100_WIDE) return from_launch(launch_attn_sm100_wide(p, d->d, d->d_v, st, dbg));
-    if (!uses_simt(d)) return from_launch(launch_attn_sm100(p, d->d, d->d_v, st, dbg));
+    if (kern == SFA_KERNEL_SM100_PAIR) return from_launch(launch_attn_sm100_pair(p, d->d, d->d_v, st, dbg));
+    if (kern == SFA_KERNEL_SM100_WIDE) return from_launch(launch_attn_sm100_wide(p, d->d, d->d_v, st, dbg));
+    if (kern == SFA_KERNEL_SM100_OT) return from_launch(launch_attn_sm100_ot(p, d->d, d->d_v, st, dbg));
+    if (kern == SFA_KERNEL_SM100) return from_launch(launch_attn_sm100(p, d->d, d->d_v, st, dbg));
     return from_cuda(launch_attn_simt(p, d->dtype == SFA_BF16, d->d, d->d_v, st));
 }
 

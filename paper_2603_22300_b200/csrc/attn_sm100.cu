@@ -245,12 +245,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_kernel(const __grid_co
                     for (int c = 0; c < 32; ++c)
                         if (32 * q + c >= lim) s[q][c] = 0xFF800000u;
             }
+#ifdef SFA_MAXTREE
+            float mq[4];  // four independent FMNMX3 chains instead of one 64-deep chain
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                mq[q] = -INFINITY;
+#pragma unroll
+                for (int c = 0; c < 32; ++c) mq[q] = fmaxf(mq[q], __uint_as_float(s[q][c]));
+            }
+            float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3]));
+#else
             float mx = -INFINITY;
 #pragma unroll
             for (int q = 0; q < 4; ++q)
 #pragma unroll
                 for (int c = 0; c < 32; ++c) mx = fmaxf(mx, __uint_as_float(s[q][c]));
+#endif
             mx *= cs;
+            if (lane == 0 && wq == 0) TLREC(0x4000 | (t << 10) | (j & 1023));
             const float m_new = fmaxf(m, mx);
             const bool need = m_new > m + 8.f;
             const bool rescale = __any_sync(0xffffffffu, need);  // warp-uniform (tcgen05.ld/st are warp-wide)
@@ -267,8 +279,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_kernel(const __grid_co
                 uint32_t pk[16];
 #pragma unroll
                 for (int c = 0; c < 16; ++c) {
-                    const float p0 = fast_exp2(fmaf(__uint_as_float(s[q][2 * c]), cs, -ms));
-                    const float p1 = fast_exp2(fmaf(__uint_as_float(s[q][2 * c + 1]), cs, -ms));
+                    const float x0 = fmaf(__uint_as_float(s[q][2 * c]), cs, -ms);
+                    const float x1 = fmaf(__uint_as_float(s[q][2 * c + 1]), cs, -ms);
+                    float p0, p1;
+#if defined(SFA_V1_POLY)
+                    if ((c & 3) < SFA_V1_POLY) {
+                        exp2_poly2(x0, x1, p0, p1);
+                    } else
+#endif
+                    {
+                        p0 = fast_exp2(x0);
+                        p1 = fast_exp2(x1);
+                    }
                     rs += p0 + p1;
                     pk[c] = pack_f16x2(p0, p1);
                 }

@@ -1,0 +1,508 @@
+// attn_sm100_ot.cu -- FlashSFA forward on sm_100a tensor cores with a TRANSPOSED output accumulator
+// (steps 4-8 of DESIGN.md; Alg. 1, Sec. 3.2).  SFA_KERNEL_SM100_OT.
+//
+// Same computation as attn_sm100.cu (scores = dense contraction of the decompressed k-sparse rows,
+// reading A1/R1; fp16 P x 2^7 against the per-head scaled fp16 V copy, reading A12; lazy O rescale),
+// laid out so that every P.V tensor-core instruction has N = 256:
+//
+//   S_t(j)   = Q~_t K~(j)^T             M = 128 query rows, N = 128 keys, K = d        (SS, per tile t)
+//   O^T     += V(j)^T [P_0(j) ; P_1(j)]^T  M = d_v = 128,  N = 256 queries of BOTH tiles, K = 128 keys
+//
+// tools/umma_bench.cu: an M = 128 instruction costs ~75-100 clocks for any N <= 128 but N = 256 runs
+// at the full 8192 FLOP/clk/SM (profiles/r01_umma_microbench.txt), so the P.V half of the tensor
+// work drops from 16 x ~100 to 8 x 128 clocks per key tile, and the two tiles' S MMAs are issued
+// interleaved (two accumulators: ~75 clk each).  P goes to shared memory (the B operand of the
+// transposed product), so S_t's TMEM columns are free as soon as the softmax has read them and
+// S_t(j+1) runs on the tensor pipe while the softmax of tile j computes its exponentials: no
+// softmax -> MMA -> softmax chain per tile as in attn_sm100.cu.
+//
+// Warp roles (512 threads):
+//   warps 0-3   softmax for query tile 0 (thread = query row = TMEM lane of S_0); with warps 4-7
+//   warps 4-7   softmax for query tile 1        they also rescale O^T columns and run the epilogue
+//   warps 8-11  decompression of Q~ (once) and K~(j) from the key codes into a 2-stage ring
+//   warp 12     tcgen05.mma issuer (one thread) + TMEM owner
+//   warp 13     TMA producer for V (single stage)
+// TMEM (512 columns): S_0 [0,128), S_1 [128,256), O^T [256,512) (lane = output feature, column =
+// query: tile 0's 128 queries then tile 1's).
+// Shared memory (d = 128): Q~ 2 x 32 KB, K~ 2 x 32 KB, V 32 KB, P 64 KB (256 rows x 128 keys fp16,
+// K-major SW128), 1 KB per-query factors; 226 KB of the 227 KB.
+#include <cudaTypedefs.h>
+#include <mutex>
+
+#include "densify.cuh"
+#include "launch.cuh"
+#include "sm100.cuh"
+
+namespace sfa {
+using namespace sm100;
+using namespace dz;
+
+namespace {
+
+constexpr int BM = 128;  // query rows per tile (UMMA M of S)
+constexpr int BN = 128;  // keys per tile (UMMA N of S, UMMA K of P.V)
+constexpr int DV = 128;  // output features (UMMA M of O^T)
+constexpr int NTHREADS = 512;
+
+template <int D>
+struct Cfg {
+    static constexpr int QT = BM * D * 2;  // one decompressed Q~ tile
+    static constexpr int KT = BN * D * 2;  // one K~ stage
+    static constexpr int VT = BN * DV * 2; // the V stage
+    static constexpr int PT = 2 * BM * BN * 2;  // P of both query tiles
+    static constexpr int OFF_Q = 0;
+    static constexpr int OFF_K = OFF_Q + 2 * QT;
+    static constexpr int OFF_V = OFF_K + 2 * KT;
+    static constexpr int OFF_P = OFF_V + VT;
+    static constexpr int OFF_BAR = OFF_P + PT;
+    static constexpr int OFF_F = OFF_BAR + 128;  // 2 x 128 fp32 per-query factors (alpha, then 1/l)
+    static constexpr int SMEM = OFF_F + 1024 + 1024;  // + slack to align the base to 1024 B
+    static constexpr int O_COL = 256;
+};
+static_assert(Cfg<128>::SMEM <= 232448, "shared memory budget");
+
+// mbarrier slots
+enum {
+    KFULL = 0, KEMPTY = 2, VFULL = 4, VEMPTY = 5, SFULL = 6, SEMPTY = 8, PFULL = 10, PEMPTY = 11, OFULL = 12,
+    QFULL = 13, NBAR = 14
+};
+
+struct OtArgs {
+    AttnParams p;
+    int32_t nqb;         // ceil(n_q / BM)
+    int32_t pair_heads;  // 1: tiles (2hp, 2hp+1) at one q block; 0: (h, 2p), (h, 2p+1)
+    int32_t per_rank;    // work items per q-block rank
+    int32_t nkt;         // ceil(n_kv / BN)
+    float c_scale;       // scale * log2(e)
+    float *dbg;          // optional: raw S of the first key tile of work item 0, tile 0 (tests)
+};
+
+constexpr float P_SHIFT = 7.f;  // P stored as fp16 * 2^7 (attn_sm100.cu, reading A12)
+
+// exponentials per group of 4 pairs computed by exp2_poly2 on the FMA pipe instead of MUFU.EX2
+// (16 ex2 / clk / SM on B200, tools/mufu_bench.cu): 1 -> 25 % (7.29 -> 6.87 ms at Qwen3-32K; 2 -> slower)
+#ifndef SFA_OT_POLY
+#define SFA_OT_POLY 1
+#endif
+
+struct Tile {
+    int h, qb;
+    bool valid;
+};
+
+__device__ __forceinline__ void decode_item(const OtArgs &a, int item, int &b, Tile (&t)[2]) {
+    const AttnParams &p = a.p;
+    const int rank = item / a.per_rank, rest = item % a.per_rank;
+    if (a.pair_heads) {
+        const int qb = a.nqb - 1 - rank;  // heaviest causal blocks first (LPT)
+        const int hp2 = p.H / 2;
+        b = rest / hp2;
+        const int hp = rest % hp2;
+        t[0] = {2 * hp, qb, true};
+        t[1] = {2 * hp + 1, qb, true};
+    } else {
+        const int npairs = (a.nqb + 1) / 2;
+        const int pr = npairs - 1 - rank;
+        b = rest / p.H;
+        const int h = rest % p.H;
+        t[0] = {h, 2 * pr, 2 * pr < a.nqb};
+        t[1] = {h, 2 * pr + 1, 2 * pr + 1 < a.nqb};
+    }
+}
+
+#ifdef SFA_TIMELINE
+#define TLREC(tag)                                                                                   \
+    do {                                                                                             \
+        if (a.dbg != nullptr && blockIdx.x == 0) {                                                   \
+            unsigned long long *tb_ = reinterpret_cast<unsigned long long *>(a.dbg + BM * BN);       \
+            const unsigned slot_ = ((((tag) >> 12) - 1) << 10) | ((((tag) >> 10) & 1) << 9) | ((tag) & 511); \
+            if (slot_ < 8191) tb_[1 + slot_] = ((unsigned long long)(tag) << 48) | (clock64() & 0xFFFFFFFFFFFFull); \
+        }                                                                                            \
+    } while (0)
+#else
+#define TLREC(tag) do {} while (0)
+#endif
+
+template <int D, bool DBG>
+__global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid_constant__ CUtensorMap tmap_v,
+                                                                      const OtArgs a) {
+    using C = Cfg<D>;
+    const AttnParams &p = a.p;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_s = smem_u32(smem_raw);
+    const uint32_t sbase = (raw_s + 1023u) & ~1023u;
+    uint8_t *gbase = smem_raw + (sbase - raw_s);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t bar0 = sbase + C::OFF_BAR;
+#define BAR(i) (bar0 + 8u * (uint32_t)(i))
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + C::OFF_BAR + 120);
+    float *fac = reinterpret_cast<float *>(gbase + C::OFF_F);
+
+    int b;
+    Tile tl[2];
+    decode_item(a, blockIdx.x, b, tl);
+    const int g = tl[0].h / (p.H / p.H_kv);
+    int nt = a.nkt;
+    if (p.causal) {
+        const int qbl = tl[1].valid ? tl[1].qb : tl[0].qb;
+        int64_t last = (int64_t)qbl * BM + BM - 1;
+        if (last > p.n_q - 1) last = p.n_q - 1;
+        const int64_t lim = (p.q_pos0 + last) / BN + 1;
+        if (lim < nt) nt = (int)lim;
+    }
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NBAR; ++i) {
+            uint32_t cnt = 1;
+            if (i == KFULL || i == KFULL + 1 || i == SEMPTY || i == SEMPTY + 1 || i == QFULL) cnt = 4;
+            if (i == PFULL) cnt = 8;
+            mbar_init(BAR(i), cnt);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 12) tmem_alloc<512>(smem_u32(tmem_slot));
+    if (warp == 13 && lane == 0) tma_prefetch_desc(&tmap_v);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const int wg = warp >> 2;
+    if (wg < 2) {
+        reg_alloc<184>();
+        // ============================ softmax (steps 5, 6, 8) ============================
+        const int t = wg, wq = warp & 3, r = wq * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+        const uint32_t tS = tmem + lane_off + (uint32_t)(t * 128);
+        // O^T: this thread's TMEM lane is output feature r; tile t's queries are columns [128t, 128t+128)
+        const uint32_t tO = tmem + lane_off + (uint32_t)(C::O_COL + t * BM);
+        const int64_t i = (int64_t)tl[t].qb * BM + r;
+        const bool row_ok = tl[t].valid && i < p.n_q;
+        int64_t kend = p.n_kv;
+        if (p.causal && p.q_pos0 + i + 1 < kend) kend = p.q_pos0 + i + 1;
+        const float cs = a.c_scale;
+        float *f_t = fac + t * BM;
+        const uint32_t prow = sbase + C::OFF_P + (uint32_t)(t * BM + r) * 128u;  // row t*128+r, key atom 0
+        const int bar_id = 1 + t;
+        float m = -INFINITY, l = 0.f;
+        for (int j = 0; j < nt; ++j) {
+            mbar_wait(BAR(SFULL + t), j & 1);
+            if (lane == 0 && wq == 0) TLREC(0x1000 | (t << 10) | (j & 1023));
+            tc_fence_after();
+            uint32_t s[4][32];
+            int64_t lim64 = kend - (int64_t)j * BN;
+            const int lim = lim64 < 0 ? 0 : (lim64 > BN ? BN : (int)lim64);
+            float mq[4];  // four independent max chains; keys 64-127 load while 0-63 are reduced
+            tmem_ld32(tS, s[0]);
+            tmem_ld32(tS + 32, s[1]);
+            tmem_ld_wait();
+            tmem_ld32(tS + 64, s[2]);
+            tmem_ld32(tS + 96, s[3]);
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                mq[q] = -INFINITY;
+#pragma unroll
+                for (int c = 0; c < 32; ++c) mq[q] = fmaxf(mq[q], __uint_as_float(s[q][c]));
+            }
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(BAR(SEMPTY + t));  // S_t may be overwritten by S_t(j+1)
+#pragma unroll
+            for (int q = 2; q < 4; ++q) {
+                mq[q] = -INFINITY;
+#pragma unroll
+                for (int c = 0; c < 32; ++c) mq[q] = fmaxf(mq[q], __uint_as_float(s[q][c]));
+            }
+            if (DBG && blockIdx.x == 0 && t == 0 && j == 0) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) a.dbg[r * BN + 32 * q + c] = __uint_as_float(s[q][c]);
+            }
+            if (lim < BN) {  // step 5 on diagonal / ragged tiles: excluded keys -> -inf -> p = 0
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    mq[q] = -INFINITY;
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        if (32 * q + c >= lim) s[q][c] = 0xFF800000u;
+                        mq[q] = fmaxf(mq[q], __uint_as_float(s[q][c]));
+                    }
+                }
+            }
+            const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * cs;
+            if (lane == 0 && wq == 0) TLREC(0x5000 | (t << 10) | (j & 1023));
+            const float m_new = fmaxf(m, mx);
+            // O^T columns are shared by the whole warpgroup: rescale all of tile t or none of it
+            const bool rescale = named_bar_or(bar_id, 128, m_new > m + 8.f);
+            if (lane == 0 && wq == 0) TLREC(0x6000 | (t << 10) | (j & 1023));
+            if (rescale) {
+                const float alpha = (m_new == -INFINITY) ? 1.f : fast_exp2(m - m_new);
+                l *= alpha;
+                m = m_new;
+                if (j > 0) f_t[r] = alpha;
+            }
+            const float ms = ((m == -INFINITY) ? 0.f : m) - P_SHIFT;  // p = 2^(s - m + P_SHIFT)
+            float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {  // keys [64h, 64h + 64) = P atom h
+                uint32_t pk[32];
+#pragma unroll
+                for (int q = 2 * h; q < 2 * h + 2; ++q) {
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        float x0, x1, p0, p1;
+                        ffma2(x0, x1, __uint_as_float(s[q][2 * c]), __uint_as_float(s[q][2 * c + 1]), cs, -ms);
+                        if ((c & 3) < SFA_OT_POLY) {  // 1 pair in 4 on the FMA pipe (exp2_poly2)
+                            exp2_poly2(x0, x1, p0, p1);
+                        } else
+                        {
+                            p0 = fast_exp2(x0);
+                            p1 = fast_exp2(x1);
+                        }
+                        fadd2(rs0, rs1, p0, p1);
+                        pk[16 * (q - 2 * h) + c] = pack_f16x2(p0, p1);
+                    }
+                }
+                if (h == 0) {
+                    if (lane == 0 && wq == 0) TLREC(0x4000 | (t << 10) | (j & 1023));
+                    // P(j-1) consumed and O^T += V(j-1)^T P(j-1)^T complete
+                    mbar_wait(BAR(PEMPTY), (j & 1) ^ 1);
+                    if (lane == 0 && wq == 0) TLREC(0x7000 | (t << 10) | (j & 1023));
+                    if (rescale && j > 0) {
+                        named_bar_sync(bar_id, 128);  // every row's alpha is in f_t
+                        tc_fence_after();
+#pragma unroll 1
+                        for (int q = 0; q < BM / 32; ++q) {
+                            uint32_t o[32];
+                            tmem_ld32(tO + 32 * q, o);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int c = 0; c < 32; c += 4) {
+                                const float4 al = *reinterpret_cast<const float4 *>(f_t + 32 * q + c);
+                                o[c + 0] = __float_as_uint(__uint_as_float(o[c + 0]) * al.x);
+                                o[c + 1] = __float_as_uint(__uint_as_float(o[c + 1]) * al.y);
+                                o[c + 2] = __float_as_uint(__uint_as_float(o[c + 2]) * al.z);
+                                o[c + 3] = __float_as_uint(__uint_as_float(o[c + 3]) * al.w);
+                            }
+                            tmem_st32(tO + 32 * q, o);
+                        }
+                        tmem_st_wait();
+                    }
+                }
+                // P row (t*128 + r), atom h: 16-byte chunk c8 swizzled by row
+#pragma unroll
+                for (int c8 = 0; c8 < 8; ++c8)
+                    sts_v4(prow + (uint32_t)h * (2 * BM * 128) + ((uint32_t)(c8 ^ (r & 7)) << 4), pk[4 * c8], pk[4 * c8 + 1],
+                           pk[4 * c8 + 2], pk[4 * c8 + 3]);
+            }
+            l += rs0 + rs1;
+            fence_proxy_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(BAR(PFULL));
+            if (lane == 0 && wq == 0) TLREC(0x2000 | (t << 10) | (j & 1023));
+        }
+        // ---- epilogue (step 8): O = 2^e (sum_j P'_j V'_j) / l, V' = V 2^-e (vprep.cu)
+        mbar_wait(BAR(OFULL), 0);
+        tc_fence_after();
+        const float inv = l > 0.f ? __uint_as_float((uint32_t)(127 + vprep_head_exp(__ldg(p.v_amax + b * p.H_kv + g))) << 23) / l : 0.f;
+        f_t[r] = inv;
+        named_bar_sync(bar_id, 128);
+        // O^T lane r = feature r: scale column c by 1/l of query c, transpose through shared memory
+        // (the dead P buffer; row = query, 16-byte chunk swizzled by row) for row-contiguous stores
+        const uint32_t so = sbase + C::OFF_P + (uint32_t)t * (BM * DV * 2);
+#pragma unroll 1
+        for (int q = 0; q < BM / 32; ++q) {
+            uint32_t o[32];
+            tmem_ld32(tO + 32 * q, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                const int qq = 32 * q + c;
+                const float v = __uint_as_float(o[c]) * f_t[qq];
+                const uint32_t addr = so + (uint32_t)qq * (DV * 2) + ((uint32_t)((r >> 3) ^ (qq & 15)) << 4) + (uint32_t)(r & 7) * 2;
+                sts_u16(addr, __bfloat16_as_ushort(__float2bfloat16_rn(v)));
+            }
+        }
+        named_bar_sync(bar_id, 128);
+        const int64_t orow = ((int64_t)b * p.H + tl[t].h) * p.n_q + i;
+        if (row_ok) {
+            uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<uint16_t *>(p.o) + orow * DV);
+#pragma unroll
+            for (int c = 0; c < DV / 8; ++c) dst[c] = lds_v4(so + (uint32_t)r * (DV * 2) + ((uint32_t)(c ^ (r & 15)) << 4));
+            p.lse[orow] = l > 0.f ? (m + __log2f(l) - P_SHIFT) * 0.69314718055994530942f : -INFINITY;
+        }
+    } else if (wg == 2) {
+        reg_dealloc<64>();
+        // ============================ decompression of Q~ and K~ ============================
+        const int r = threadIdx.x - 256;
+        const int k = p.k;
+        const uint16_t *qv = reinterpret_cast<const uint16_t *>(p.q_val);
+        const uint16_t *kv = reinterpret_cast<const uint16_t *>(p.k_val);
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int64_t i = (int64_t)tl[t].qb * BM + r;
+            const bool ok = tl[t].valid && i < p.n_q;
+            const int64_t row = ((int64_t)b * p.H + tl[t].h) * p.n_q + i;
+            densify_row<D>(sbase + C::OFF_Q + t * C::QT, BM, r, ok, p.q_idx + row * k, qv + row * k, k);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(QFULL));
+        const int64_t kv0 = ((int64_t)b * p.H_kv + g) * p.n_kv;
+        for (int j = 0; j < nt; ++j) {
+            const int s = j & 1, u = j >> 1;
+            const int64_t key = (int64_t)j * BN + r;
+            const bool ok = key < p.n_kv;
+            mbar_wait(BAR(KEMPTY + s), (u & 1) ^ 1);
+            densify_row<D>(sbase + C::OFF_K + s * C::KT, BN, r, ok, p.k_idx + (kv0 + key) * k, kv + (kv0 + key) * k, k);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(BAR(KFULL + s));
+        }
+    } else {
+        reg_dealloc<80>();
+        if (warp == 12) {
+            // ============================ tcgen05.mma issuer ============================
+            if (lane == 0) {
+                constexpr uint32_t idS = umma_idesc_f16kind(BM, BN, 0, 0, 1);      // bf16 Q~ x bf16 K~
+                constexpr uint32_t idO = umma_idesc_f16kind(DV, 2 * BM, 1, 0, 0);  // fp16 V^T (MN-major) x fp16 P
+                auto mma_S = [&](int s) {  // both tiles, instruction by instruction (two accumulators)
+                    const uint32_t ka = sbase + C::OFF_K + s * C::KT;
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint32_t off_q = (kk >> 2) * BM * 128 + (kk & 3) * 32;
+                        const uint32_t off_k = (kk >> 2) * BN * 128 + (kk & 3) * 32;
+                        const uint64_t kd = umma_desc_sw128(ka + off_k, 16, 1024);
+#pragma unroll
+                        for (int t = 0; t < 2; ++t)
+                            umma_ss(tmem + t * 128, umma_desc_sw128(sbase + C::OFF_Q + t * C::QT + off_q, 16, 1024), kd,
+                                    idS, kk > 0);
+                    }
+                };
+                auto mma_O = [&](bool acc) {
+                    const uint32_t va = sbase + C::OFF_V, pa = sbase + C::OFF_P;
+#pragma unroll
+                    for (int kk = 0; kk < BN / 16; ++kk)
+                        umma_ss(tmem + C::O_COL, umma_desc_sw128(va + kk * 2048, BN * 128, 1024),
+                                umma_desc_sw128(pa + (kk >> 2) * (2 * BM * 128) + (kk & 3) * 32, 16, 1024), idO,
+                                (acc || kk > 0) ? 1u : 0u);
+                };
+                mbar_wait(BAR(QFULL), 0);
+                mbar_wait(BAR(KFULL + 0), 0);
+                tc_fence_after();
+                mma_S(0);
+                umma_commit(BAR(SFULL + 0));
+                umma_commit(BAR(SFULL + 1));
+                umma_commit(BAR(KEMPTY + 0));
+                for (int j = 0; j < nt; ++j) {
+                    if (j + 1 < nt) {
+                        const int s1 = (j + 1) & 1, u1 = (j + 1) >> 1;
+                        mbar_wait(BAR(KFULL + s1), u1 & 1);
+                        mbar_wait(BAR(SEMPTY + 0), j & 1);
+                        mbar_wait(BAR(SEMPTY + 1), j & 1);
+                        tc_fence_after();
+                        mma_S(s1);
+                        umma_commit(BAR(SFULL + 0));
+                        umma_commit(BAR(SFULL + 1));
+                        umma_commit(BAR(KEMPTY + s1));
+                    }
+                    mbar_wait(BAR(VFULL), j & 1);
+                    mbar_wait(BAR(PFULL), j & 1);
+                    TLREC(0x3000 | (j & 1023));
+                    tc_fence_after();
+                    mma_O(j > 0);
+                    umma_commit(BAR(PEMPTY));
+                    umma_commit(BAR(VEMPTY));
+                }
+                umma_commit(BAR(OFULL));
+            }
+            __syncwarp();
+        } else if (warp == 13) {
+            // ============================ TMA producer for V ============================
+            if (lane == 0) {
+                const int bhkv = b * p.H_kv + g;
+                for (int j = 0; j < nt; ++j) {
+                    mbar_wait(BAR(VEMPTY), (j & 1) ^ 1);
+                    mbar_arrive_expect_tx(BAR(VFULL), C::VT);
+                    const uint32_t dst = sbase + C::OFF_V;
+#pragma unroll
+                    for (int cb = 0; cb < DV / 64; ++cb)
+                        tma_load_3d(dst + cb * BN * 128, &tmap_v, BAR(VFULL), cb * 64, j * BN, bhkv);
+                }
+            }
+            __syncwarp();
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 12) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+#undef BAR
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void *f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+template <int D>
+cudaError_t launch_t(const OtArgs &a, cudaStream_t stream, int items) {
+    using C = Cfg<D>;
+    const AttnParams &p = a.p;
+    auto encode = get_encode();
+    if (!encode) return cudaErrorNotSupported;
+    CUtensorMap tm;
+    cuuint64_t dims[3] = {(cuuint64_t)DV, (cuuint64_t)p.n_kv, (cuuint64_t)p.B * p.H_kv};
+    cuuint64_t strides[2] = {(cuuint64_t)DV * 2, (cuuint64_t)p.n_kv * DV * 2};
+    cuuint32_t box[3] = {64, BN, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult cr = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void *>(p.v16), dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    auto kern = a.dbg != nullptr ? attn_sm100_ot_kernel<D, true> : attn_sm100_ot_kernel<D, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    kern<<<items, NTHREADS, C::SMEM, stream>>>(tm, a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_attn_sm100_ot(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg) {
+    if ((d != 64 && d != 128) || d_v != DV) return cudaErrorNotSupported;
+    OtArgs a;
+    a.p = p;
+    a.nqb = (int)((p.n_q + BM - 1) / BM);
+    a.nkt = (int)((p.n_kv + BN - 1) / BN);
+    a.c_scale = p.scale_log2;
+    a.dbg = dbg;
+    const int R = p.H / p.H_kv;
+    a.pair_heads = (R % 2 == 0) ? 1 : 0;
+    int64_t items;
+    if (a.pair_heads) {
+        a.per_rank = p.B * (p.H / 2);
+        items = (int64_t)a.per_rank * a.nqb;
+    } else {
+        a.per_rank = p.B * p.H;
+        items = (int64_t)a.per_rank * ((a.nqb + 1) / 2);
+    }
+    if (items == 0) return cudaSuccess;
+    if (items > INT32_MAX) return cudaErrorNotSupported;
+    return d == 64 ? launch_t<64>(a, stream, (int)items) : launch_t<128>(a, stream, (int)items);
+}
+
+}  // namespace sfa

@@ -47,5 +47,6 @@ cudaError_t launch_attn_sm100(const AttnParams &p, int d, int d_v, cudaStream_t 
 cudaError_t launch_attn_sm100_pair(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
 // the same forward with 256-key score tiles and P apart from S (attn_sm100_wide.cu)
 cudaError_t launch_attn_sm100_wide(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
+cudaError_t launch_attn_sm100_ot(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
 
 }  // namespace sfa

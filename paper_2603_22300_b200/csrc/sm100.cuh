@@ -155,6 +155,24 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
+// named barrier that also returns the OR of `pred` over the `count` participating threads
+__device__ __forceinline__ bool named_bar_or(int id, int count, bool pred) {
+    uint32_t r;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\tsetp.ne.u32 q, %1, 0;\n\tbar.red.or.pred p, %2, %3, q;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(r)
+        : "r"((uint32_t)pred), "r"(id), "r"(count)
+        : "memory");
+    return r != 0;
+}
+__device__ __forceinline__ void sts_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+    return v;
+}
 
 
 // ---- CTA pairs (cluster of 2, tcgen05 cta_group::2) ----------------------------------------------
@@ -250,6 +268,24 @@ __device__ __forceinline__ void ffma2v(float &d0, float &d1, float a0, float a1,
         "mov.b64 rc, {%6, %7};\n\tfma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
         : "=f"(d0), "=f"(d1)
         : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+
+// 2^x for two values on the FMA pipe instead of MUFU (FA4-style offload): round-to-nearest split
+// x = n + f (|f| <= 1/2) by the 1.5 * 2^23 shifter, 2^f by a degree-3 minimax polynomial (max relative
+// error 7.5e-5, below the fp16 half-ulp 2.4e-4 of the P it feeds), 2^n added into the exponent field.
+// x is clamped to >= -125 so the result stays a normal float (weights below 2^-125 are 0 in fp16 P).
+__device__ __forceinline__ void exp2_poly2(float x0, float x1, float &y0, float &y1) {
+    x0 = fmaxf(x0, -125.f);
+    x1 = fmaxf(x1, -125.f);
+    float t0, t1, r0, r1, f0, f1, p0, p1;
+    ffma2(t0, t1, x0, x1, 1.f, 12582912.f);      // t = x + 1.5*2^23: n = round(x) in the low bits
+    ffma2(r0, r1, t0, t1, 1.f, -12582912.f);     // r = n
+    ffma2v(f0, f1, r0, r1, -1.f, -1.f, x0, x1);  // f = x - n
+    ffma2(p0, p1, f0, f1, 0.05517132207751274f, 0.24261054396629333f);
+    ffma2v(p0, p1, p0, p1, f0, f1, 0.6932609677314758f, 0.6932609677314758f);
+    ffma2v(p0, p1, p0, p1, f0, f1, 0.9999281167984009f, 0.9999281167984009f);
+    y0 = __uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23));
+    y1 = __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23));
 }
 
 __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {

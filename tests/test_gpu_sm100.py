@@ -83,11 +83,11 @@ def test_peaked_rows_trigger_rescale(lib):
 # ---------------------------------------------------------------------------------------------
 # M = 256 CTA-pair kernel (attn_sm100_pair.cu): same checks
 # ---------------------------------------------------------------------------------------------
-VARIANTS = ["pair", "wide"]  # SFA_KERNEL_SM100_PAIR / SFA_KERNEL_SM100_WIDE
+VARIANTS = ["pair", "wide", "ot"]  # SFA_KERNEL_SM100_PAIR / _WIDE / _OT
 
 
 def _kern(lib, name):
-    return {"pair": lib.KERNEL_SM100_PAIR, "wide": lib.KERNEL_SM100_WIDE}[name]
+    return {"pair": lib.KERNEL_SM100_PAIR, "wide": lib.KERNEL_SM100_WIDE, "ot": lib.KERNEL_SM100_OT}[name]
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
@@ -120,8 +120,8 @@ def test_variant_score_tile_is_exact_overlap_sum(lib, variant, d, k):
 def test_variant_against_oracle(lib, variant, shape, causal):
     import torch
     B, H, H_kv, n, d, d_v, k = shape
-    if variant == "pair" and d_v != 128:
-        pytest.skip("the pair kernel splits d_v = 128 over the CTA pair")
+    if variant in ("pair", "ot") and d_v != 128:
+        pytest.skip("pair / ot kernels need d_v = 128 (M of the transposed product / split over the pair)")
     q, kx, v = host_qkv(56, B, H, H_kv, n, d, d_v, "bf16")
     qi, qv = oracle_codes(q, k)
     ki, kv = oracle_codes(kx, k)
