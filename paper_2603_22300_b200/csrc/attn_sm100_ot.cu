@@ -44,15 +44,7 @@ namespace {
 #ifndef SFA_OT_POLY
 #define SFA_OT_POLY 1
 #endif
-// 1: Q~ in TMEM (S = Q~ K~^T as TS-MMAs through ONE 128-column S buffer used by the two tiles in
-//    turn); 0: Q~ in shared memory, S_0 and S_1 in TMEM (SS-MMAs)
-#ifndef SFA_OT_QTMEM
-#define SFA_OT_QTMEM 0
-#endif
-// QTMEM issue order: 0 = S_1(j), P.V(j-1), S_0(j+1); 1 = S_1(j), S_0(j+1), P.V(j-1)
-#ifndef SFA_OT_PVLATE
-#define SFA_OT_PVLATE 0
-#endif
+
 
 constexpr int BM = 128;  // query rows per tile (UMMA M of S)
 constexpr int BN = 128;  // keys per tile (UMMA N of S, UMMA K of P.V)
@@ -65,22 +57,17 @@ struct Cfg {
     static constexpr int KT = BN * D * 2;  // one K~ stage
     static constexpr int VT = BN * DV * 2; // the V stage
     static constexpr int PT = 2 * BM * BN * 2;  // P of both query tiles
-#if SFA_OT_QTMEM
-    static constexpr int OFF_K = 0;  // Q~ lives in TMEM (staged once through the P buffer)
-#else
     static constexpr int OFF_Q = 0;
     static constexpr int OFF_K = OFF_Q + 2 * QT;
-#endif
-    static constexpr int NV = SFA_OT_QTMEM ? 2 : 1;  // V stages
-    static constexpr int NK = SFA_OT_QTMEM ? 1 : 2;  // K~ stages
-    static constexpr int NP = SFA_OT_QTMEM ? 2 : 1;  // P stages
+    static constexpr int NV = 1;  // V stages
+    static constexpr int NK = 2;  // K~ stages
+    static constexpr int NP = 1;  // P stages
     static constexpr int OFF_V = OFF_K + NK * KT;
     static constexpr int OFF_P = OFF_V + NV * VT;
     static constexpr int OFF_BAR = OFF_P + NP * PT;
     static constexpr int OFF_F = OFF_BAR + 192;  // 2 x 128 fp32 per-query factors (alpha, then 1/l)
     static constexpr int SMEM = OFF_F + 1024 + 1024;  // + slack to align the base to 1024 B
     static constexpr int O_COL = 256;
-    static constexpr int Q_COL = 128;  // SFA_OT_QTMEM: Q~_t at [128 + 64 t, ...), 2 bf16 per column
 };
 static_assert(Cfg<128>::SMEM <= 232448, "shared memory budget");
 
@@ -192,7 +179,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         // ============================ softmax (steps 5, 6, 8) ============================
         const int t = wg, wq = warp & 3, r = wq * 32 + lane;
         const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-        const uint32_t tS = tmem + lane_off + (uint32_t)(SFA_OT_QTMEM ? 0 : t * 128);
+        const uint32_t tS = tmem + lane_off + (uint32_t)(t * 128);
         // O^T: this thread's TMEM lane is output feature r; tile t's queries are columns [128t, 128t+128)
         const uint32_t tO = tmem + lane_off + (uint32_t)(C::O_COL + t * BM);
         const int64_t i = (int64_t)tl[t].qb * BM + r;
@@ -290,8 +277,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                     mbar_wait(BAR(PEMPTY + j % C::NP), ((j / C::NP) & 1) ^ 1);
                     if (lane == 0 && wq == 0) TLREC(0x7000 | (t << 10) | (j & 1023));
                     if (rescale && j > 0) {
-                        // O^T must hold exactly sum_{j' < j}: wait for O^T += V(j-1)^T P(j-1)^T
-                        if (C::NP > 1) mbar_wait(BAR(PEMPTY + (j - 1) % C::NP), ((j - 1) / C::NP) & 1);
                         named_bar_sync(bar_id, 128);  // every row's alpha is in f_t
                         tc_fence_after();
 #pragma unroll 1
@@ -362,46 +347,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         const int k = p.k;
         const uint16_t *qv = reinterpret_cast<const uint16_t *>(p.q_val);
         const uint16_t *kv = reinterpret_cast<const uint16_t *>(p.k_val);
-#if SFA_OT_QTMEM
-        {
-            // Q~ row r of both tiles -> TMEM lane r (this warp's lane quadrant), columns Q_COL + 64 t:
-            // zero + scatter into a row of the (still unused) P buffer, read it back as D/2 words
-            constexpr int NCH = D / 8;  // 16-byte chunks per row, swizzled by row
-            const uint32_t qwg = (uint32_t)(warp & 3) * 32u << 16;
-#pragma unroll
-            for (int t = 0; t < 2; ++t) {
-                const int64_t i = (int64_t)tl[t].qb * BM + r;
-                const bool ok = tl[t].valid && i < p.n_q;
-                const int64_t row = ((int64_t)b * p.H + tl[t].h) * p.n_q + i;
-                const uint32_t rb = sbase + C::OFF_P + (uint32_t)(t * BM + r) * (2 * D);
-#pragma unroll
-                for (int c = 0; c < NCH; ++c) sts_zero16(rb + ((uint32_t)c << 4));
-                if (ok)
-                    for (int c = 0; c < k; ++c) {
-                        const int f = __ldg(p.q_idx + row * k + c);
-                        sts_u16(rb + ((uint32_t)((f >> 3) ^ (r & (NCH - 1))) << 4) + (uint32_t)(f & 7) * 2,
-                                __ldg(qv + row * k + c));
-                    }
-#pragma unroll
-                for (int h = 0; h < D / 64; ++h) {
-                    uint32_t w[32];
-#pragma unroll
-                    for (int c4 = 0; c4 < 8; ++c4) {
-                        const uint4 v4 = lds_v4(rb + ((uint32_t)((h * 8 + c4) ^ (r & (NCH - 1))) << 4));
-                        w[4 * c4] = v4.x;
-                        w[4 * c4 + 1] = v4.y;
-                        w[4 * c4 + 2] = v4.z;
-                        w[4 * c4 + 3] = v4.w;
-                    }
-                    tmem_st32(tmem + qwg + (uint32_t)(C::Q_COL + 64 * t + 32 * h), w);
-                }
-            }
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(BAR(QFULL));
-        }
-#else
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
             const int64_t i = (int64_t)tl[t].qb * BM + r;
@@ -412,7 +357,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(QFULL));
-#endif
         const int64_t kv0 = ((int64_t)b * p.H_kv + g) * p.n_kv;
         for (int j = 0; j < nt; ++j) {
             const int s = j % C::NK, u = j / C::NK;
@@ -439,54 +383,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                                 umma_desc_sw128(pa + (kk >> 2) * (2 * BM * 128) + (kk & 3) * 32, 16, 1024), idO,
                                 (acc || kk > 0) ? 1u : 0u);
                 };
-#if SFA_OT_QTMEM
-                // S_t = Q~_t K~^T: Q~_t from TMEM (8 columns per K step), K~ from shared memory; one S
-                // buffer, used in the order S_0(0), S_1(0), S_0(1), ...
-                auto mma_S1 = [&](int t, int s) {
-                    const uint32_t ka = sbase + C::OFF_K + s * C::KT;
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk)
-                        umma_ts(tmem, tmem + C::Q_COL + 64 * t + 8 * kk,
-                                umma_desc_sw128(ka + (kk >> 2) * BN * 128 + (kk & 3) * 32, 16, 1024), idS, kk > 0);
-                };
-                mbar_wait(BAR(QFULL), 0);
-                mbar_wait(BAR(KFULL + 0), 0);
-                tc_fence_after();
-                mma_S1(0, 0);
-                umma_commit(BAR(SFULL + 0));
-                // issue order S_1(j), O^T += V(j-1)^T P(j-1)^T, S_0(j+1): the events they wait for
-                // (tile 0 read S_0(j), both tiles stored P(j-1), tile 1 read S_1(j)) come in that order
-                auto pv = [&](int jj) {
-                    const int vs = jj % C::NV;
-                    mbar_wait(BAR(VFULL + vs), (jj / C::NV) & 1);
-                    const int ps = jj % C::NP;
-                    mbar_wait(BAR(PFULL + ps), (jj / C::NP) & 1);
-                    TLREC(0x3000 | (jj & 1023));
-                    tc_fence_after();
-                    mma_O(jj > 0, vs, ps);
-                    umma_commit(BAR(PEMPTY + ps));
-                    umma_commit(BAR(VEMPTY + vs));
-                };
-                for (int j = 0; j < nt; ++j) {
-                    const int s = j % C::NK;
-                    mbar_wait(BAR(SEMPTY + 0), j & 1);  // tile 0 holds S_0(j) in registers
-                    tc_fence_after();
-                    mma_S1(1, s);
-                    umma_commit(BAR(SFULL + 1));
-                    umma_commit(BAR(KEMPTY + s));
-                    if (SFA_OT_PVLATE == 0 && j > 0) pv(j - 1);
-                    if (j + 1 < nt) {
-                        const int s1 = (j + 1) % C::NK, u1 = (j + 1) / C::NK;
-                        mbar_wait(BAR(KFULL + s1), u1 & 1);
-                        mbar_wait(BAR(SEMPTY + 1), j & 1);  // tile 1 holds S_1(j)
-                        tc_fence_after();
-                        mma_S1(0, s1);
-                        umma_commit(BAR(SFULL + 0));
-                    }
-                    if (SFA_OT_PVLATE == 1 && j > 0) pv(j - 1);
-                }
-                pv(nt - 1);
-#else
                 auto mma_S = [&](int s) {  // both tiles, instruction by instruction (two accumulators)
                     const uint32_t ka = sbase + C::OFF_K + s * C::KT;
 #pragma unroll
@@ -527,7 +423,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                     umma_commit(BAR(PEMPTY));
                     umma_commit(BAR(VEMPTY));
                 }
-#endif
                 umma_commit(BAR(OFULL));
             }
             __syncwarp();
