@@ -10,8 +10,9 @@
 //
 // tools/umma_bench.cu: an M = 128 instruction costs ~75-100 clocks for any N <= 128 but N = 256 runs
 // at the full 8192 FLOP/clk/SM (profiles/r01_umma_microbench.txt), so the P.V half of the tensor
-// work drops from 16 x ~100 to 8 x 128 clocks per key tile, and the two tiles' S MMAs are issued
-// interleaved (two accumulators: ~75 clk each).  P goes to shared memory (the B operand of the
+// work drops from 16 x ~100 to 8 x 128 clocks per key tile; each tile's S MMAs are issued as soon as
+// that tile has read its previous scores (issuing both tiles' S interleaved, two accumulators, was
+// ~2 % slower).  P goes to shared memory (the B operand of the
 // transposed product), so S_t's TMEM columns are free as soon as the softmax has read them and
 // S_t(j+1) runs on the tensor pipe while the softmax of tile j computes its exponentials: no
 // softmax -> MMA -> softmax chain per tile as in attn_sm100.cu.
@@ -39,11 +40,13 @@ using namespace dz;
 
 namespace {
 
-// exponentials per group of 4 pairs computed by exp2_poly2 on the FMA pipe instead of MUFU.EX2
-// (16 ex2 / clk / SM on B200, tools/mufu_bench.cu): 1 -> 25 % (7.29 -> 6.87 ms at Qwen3-32K; 2 -> slower)
+// exponentials per group of 8 pairs computed by exp2_poly2 on the FMA pipe instead of MUFU.EX2
+// (16 ex2 / clk / SM on B200, tools/mufu_bench.cu): 2 of 8 (25 %) is fastest at Qwen3-32K (1: +4 %,
+// 3: +2 %, 4: +15 %; none: +8 %)
 #ifndef SFA_OT_POLY
-#define SFA_OT_POLY 1
+#define SFA_OT_POLY 2
 #endif
+
 
 
 constexpr int BM = 128;  // query rows per tile (UMMA M of S)
@@ -260,7 +263,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                     for (int c = 0; c < 16; ++c) {
                         float x0, x1, p0, p1;
                         ffma2(x0, x1, __uint_as_float(s[q][2 * c]), __uint_as_float(s[q][2 * c + 1]), cs, -ms);
-                        if ((c & 3) < SFA_OT_POLY) {  // 1 pair in 4 on the FMA pipe (exp2_poly2)
+                        if ((c & 7) < SFA_OT_POLY) {  // SFA_OT_POLY pairs in 8 on the FMA pipe (exp2_poly2)
                             exp2_poly2(x0, x1, p0, p1);
                         } else
                         {
@@ -407,12 +410,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                     if (j + 1 < nt) {
                         const int s1 = (j + 1) & 1, u1 = (j + 1) >> 1;
                         mbar_wait(BAR(KFULL + s1), u1 & 1);
-                        mbar_wait(BAR(SEMPTY + 0), j & 1);
-                        mbar_wait(BAR(SEMPTY + 1), j & 1);
-                        tc_fence_after();
-                        mma_S(s1);
-                        umma_commit(BAR(SFULL + 0));
-                        umma_commit(BAR(SFULL + 1));
+                        const uint32_t ka = sbase + C::OFF_K + s1 * C::KT;
+#pragma unroll
+                        for (int t = 0; t < 2; ++t) {  // each tile's S as soon as that tile has read the last one
+                            mbar_wait(BAR(SEMPTY + t), j & 1);
+                            tc_fence_after();
+#pragma unroll
+                            for (int kk = 0; kk < D / 16; ++kk)
+                                umma_ss(tmem + t * 128,
+                                        umma_desc_sw128(sbase + C::OFF_Q + t * C::QT + (kk >> 2) * BM * 128 + (kk & 3) * 32, 16, 1024),
+                                        umma_desc_sw128(ka + (kk >> 2) * BN * 128 + (kk & 3) * 32, 16, 1024), idS, kk > 0);
+                            umma_commit(BAR(SFULL + t));
+                        }
                         umma_commit(BAR(KEMPTY + s1));
                     }
                     mbar_wait(BAR(VFULL), j & 1);  // NV == 1 here

@@ -1,10 +1,8 @@
 mkdir -p gpurun_out
-b() { SFA_NVCC_FLAGS="$1" python -m paper_2603_22300_b200.build --force >/dev/null; }
-bench() { timeout 300 python bench.py --steps 10 --warmup 3 --kernel $1 --no-cpu-baseline > gpurun_out/bench_$2.json 2>gpurun_out/bench_$2.err; echo "$2 rc=$? $(grep -o '"attn": [0-9.]*' gpurun_out/bench_$2.json)"; }
-b ""
-timeout 300 python -m pytest tests/test_gpu_sm100.py -m gpu -x -q -k ot > gpurun_out/t_q.log 2>&1; echo "pytest rc=$? $(tail -1 gpurun_out/t_q.log)"
-bench ot late1
-b "-DSFA_OT_PVLATE=0"
-bench ot late0
-SFA_NVCC_FLAGS="-DSFA_TIMELINE" python -m paper_2603_22300_b200.build --force >/dev/null && timeout 120 python tools/timeline.py 32768 ot qwen > gpurun_out/tl_qt.txt 2>&1
-sed -n 30,36p gpurun_out/tl_qt.txt
+python -m paper_2603_22300_b200.build --force >/dev/null
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$? $(tail -1 gpurun_out/pytest_gpu.log)"
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
+timeout 300 python bench.py > gpurun_out/bench_default.json 2>gpurun_out/bench_default.err; echo "bench rc=$?"
+grep -o '"attn": [0-9.]*' gpurun_out/bench_default.json
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_ot.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_sm100_ot -s 1 -c 1 -o gpurun_out/ot_final -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
