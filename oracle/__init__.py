@@ -21,7 +21,7 @@ _SRC = os.path.join(_HERE, "sfa_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
-F32, BF16 = 0, 1
+F32, BF16, F64 = 0, 1, 2
 
 
 def build(force: bool = False) -> str:
@@ -46,6 +46,8 @@ def _load():
         _lib.ref_attn_fwd.restype = I
         _lib.ref_scores_row.argtypes = [I, I, I, I, I, L, L, L, I, D, I, P, P, P, P, L, P]
         _lib.ref_scores_row.restype = I
+        _lib.ref_attn_bwd.argtypes = [I, I, I, I, I, I, L, L, L, I, D, I, P, P, P, P, P, P, P, P, P, P, P, P, I]
+        _lib.ref_attn_bwd.restype = I
         _lib.ref_edge_count.argtypes = [I, I, I, I, L, L, L, I, P, P]
         _lib.ref_edge_count.restype = L
     return _lib
@@ -66,7 +68,9 @@ def _dtype_code(vals: np.ndarray) -> int:
         return F32
     if vals.dtype == np.uint16:  # bf16 bit patterns
         return BF16
-    raise TypeError(f"oracle takes float32 or uint16 (bf16 bits), got {vals.dtype}")
+    if vals.dtype == np.float64:  # finite-difference pins of attn_bwd only
+        return F64
+    raise TypeError(f"oracle takes float32, float64 or uint16 (bf16 bits), got {vals.dtype}")
 
 
 def topk_codes(x: np.ndarray, k: int):
@@ -115,6 +119,38 @@ def attn_fwd(q_idx, q_val, k_idx, k_val, v, *, d, causal=True, scale=None, q_pos
     if st:
         raise OracleError(st)
     return o, lse
+
+
+def attn_bwd(q_idx, q_val, k_idx, k_val, v, dO, *, d, causal=True, scale=None, q_pos0=0, bounds=False,
+             threads=None):
+    """Plain fp64 SFA backward with the straight-through rule (sfa_oracle.c ref_attn_bwd).
+
+    Inputs as attn_fwd plus dO [B,H,n_q,d_v] (any float dtype, used as fp64).  Returns fp64
+    (dq_val [B,H,n_q,k], dk_val [B,H_kv,n_kv,k], dv [B,H_kv,n_kv,d_v]) -- the gradients with respect
+    to the code values and V -- and, with ``bounds=True``, their componentwise magnitude sums
+    (bq, bk, bv) used by the GPU tolerance (reading A24)."""
+    q_idx = np.ascontiguousarray(q_idx); q_val = np.ascontiguousarray(q_val)
+    k_idx = np.ascontiguousarray(k_idx); k_val = np.ascontiguousarray(k_val)
+    v = np.ascontiguousarray(v)
+    dO = np.ascontiguousarray(dO, dtype=np.float64)
+    B, H, n_q, k = q_idx.shape
+    _, H_kv, n_kv, _ = k_idx.shape
+    d_v = v.shape[-1]
+    dt = _dtype_code(q_val)
+    assert _dtype_code(k_val) == dt and _dtype_code(v) == dt
+    if scale is None:
+        scale = 1.0 / np.sqrt(d)
+    dq = np.zeros((B, H, n_q, k)); dk = np.zeros((B, H_kv, n_kv, k)); dv = np.zeros((B, H_kv, n_kv, d_v))
+    bq = np.zeros_like(dq) if bounds else None
+    bk = np.zeros_like(dk) if bounds else None
+    bv = np.zeros_like(dv) if bounds else None
+    threads = threads or os.cpu_count() or 1
+    st = _load().ref_attn_bwd(B, H, H_kv, d, k, d_v, n_q, n_kv, q_pos0, int(bool(causal)), float(scale), dt,
+                              _ptr(q_idx), _ptr(q_val), _ptr(k_idx), _ptr(k_val), _ptr(v), _ptr(dO), _ptr(dq),
+                              _ptr(dk), _ptr(dv), _ptr(bq), _ptr(bk), _ptr(bv), int(threads))
+    if st:
+        raise OracleError(st)
+    return (dq, dk, dv, bq, bk, bv) if bounds else (dq, dk, dv)
 
 
 def scores_row(q_idx, q_val, k_idx, k_val, flat_row, *, d, causal=True, scale=None, q_pos0=0):

@@ -32,6 +32,22 @@
  *
  *   ref_scores_row   the s_ij of one row (for the "rows of P sum to 1" pin).
  *
+ *   ref_attn_bwd     the backward pass of ref_attn_fwd with the straight-through rule
+ *                    (Sec. 3.1 "Backward computation", Eq. topk_grad: gradients
+ *                    flow only through the selected coordinates), given the upstream dO:
+ *                      P_ij = exp(s_ij - LSE_i) (s, LSE recomputed as in ref_attn_fwd)
+ *                      O_i = sum_j P_ij V_j ;  D_i = sum_c dO_ic O_ic
+ *                      dP_ij = sum_c dO_ic V_jc ;  dS_ij = P_ij (dP_ij - D_i)   (softmax Jacobian)
+ *                      dV_j  = sum_{h in group} sum_i P_ij dO_i                 (A15: GQA heads add)
+ *                      dq~_iu = scale sum_j dS_ij k~_ju ;  dk~_ju = scale sum_{h,i} dS_ij q~_iu
+ *                      dq_val[i][t] = dq~_{i, q_idx[i][t]} ; dk_val[j][t] = dk~_{j, k_idx[j][t]}
+ *                    (the gradient w.r.t. the code values; the dense dQ / dK of Eq. topk_grad are
+ *                    these scattered to the support, zero elsewhere).  Materialised rows, fp64.
+ *                    Optional companions (tests' componentwise error bounds, A24):
+ *                      bv[j][c] = sum_i P_ij |dO_ic|
+ *                      bq[i][t] = scale sum_j P_ij (|dP_ij| + |D_i| + sum_c |dO_ic|(|O_ic| + 1)) |k~_ju|
+ *                      bk[j][t] = the same with q~ in place of k~ (summed over the group's heads)
+ *
  *   ref_edge_count   E = sum_i sum_{allowed j} |S_i (intersect) S_j|  -- the number of
  *                    structural intersections ("Efficiency analysis"),
  *                    counted pair by pair.
@@ -43,7 +59,7 @@
  * example 6/sqrt(4) = 3.0; prefix-count edge formula and the balanced-support closed
  * form n^2 k^2 / d.
  *
- * Dtypes: 0 = fp32, 1 = bf16 (IEEE bit patterns, widened exactly to double).
+ * Dtypes: 0 = fp32, 1 = bf16 (IEEE bit patterns, widened exactly to double), 2 = fp64 (gradient pins).
  * Layouts (row-major, last index fastest):
  *   x      [rows][d]          q_idx/q_val [B][H][n_q][k]     k_idx/k_val [B][H_kv][n_kv][k]
  *   v      [B][H_kv][n_kv][d_v]                              o [nsel][d_v] fp64, lse [nsel] fp64
@@ -59,6 +75,11 @@ enum { ORACLE_OK = 0, ORACLE_INVALID_ARGUMENT = 1, ORACLE_INVALID_INPUT = 2 };
 
 /* ---- value widening (exact) ------------------------------------------------------ */
 static double widen(const void *base, int dtype, int64_t i) {
+    if (dtype == 2) { /* fp64 values: only for the finite-difference pins of ref_attn_bwd */
+        double x;
+        memcpy(&x, (const char *)base + 8 * i, 8);
+        return x;
+    }
     if (dtype == 0) {
         float f;
         memcpy(&f, (const char *)base + 4 * i, 4);
@@ -75,7 +96,7 @@ static double widen(const void *base, int dtype, int64_t i) {
 }
 
 static void copy_elem(void *dst, int64_t di, const void *src, int64_t si, int dtype) {
-    size_t s = dtype == 0 ? 4 : 2;
+    size_t s = dtype == 2 ? 8 : (dtype == 0 ? 4 : 2);
     memcpy((char *)dst + s * di, (const char *)src + s * si, s);
 }
 
@@ -201,7 +222,7 @@ int ref_attn_fwd(int B, int H, int H_kv, int d, int k, int d_v, int64_t n_q, int
                  const uint8_t *k_idx, const void *k_val, const void *v, const int64_t *sel, int64_t nsel,
                  double *o, double *lse, int threads) {
     if (B < 1 || H < 1 || H_kv < 1 || H % H_kv || d < 1 || d > 256 || k < 1 || k > d || d_v < 1 || n_q < 0 ||
-        n_kv < 0 || (dtype != 0 && dtype != 1) || !(scale > 0) || !isfinite(scale))
+        n_kv < 0 || dtype < 0 || dtype > 2 || !(scale > 0) || !isfinite(scale))
         return ORACLE_INVALID_ARGUMENT;
     attn_job J;
     memset(&J, 0, sizeof J);
@@ -263,4 +284,155 @@ int64_t ref_edge_count(int B, int H, int H_kv, int k, int64_t n_q, int64_t n_kv,
             }
         }
     return E;
+}
+
+/* ---- backward with the straight-through rule: P:L103-112 ----------------------------- */
+typedef struct {
+    int B, H, H_kv, d, k, d_v, causal, dtype;
+    int64_t n_q, n_kv, q_pos0;
+    double scale;
+    const uint8_t *q_idx, *k_idx;
+    const void *q_val, *k_val, *v;
+    const double *dO;                 /* [B][H][n_q][d_v] fp64 */
+    double *dq, *dk, *dv;             /* [B][H][n_q][k], [B][H_kv][n_kv][k], [B][H_kv][n_kv][d_v] */
+    double *bq, *bk, *bv;             /* nullable bounds, same shapes */
+    int64_t next;                     /* work cursor over (b, kv head) groups */
+    pthread_mutex_t mu;
+    int status;
+} bwd_job;
+
+/* one (b, kv head g): all R query heads of the group, so dK~ / dV of the group are owned here */
+static int bwd_group(bwd_job *J, int b, int g) {
+    const int R = J->H / J->H_kv, d = J->d, k = J->k, dv = J->d_v;
+    const int64_t nq = J->n_q, nkv = J->n_kv;
+    const int64_t kvrow0 = ((int64_t)b * J->H_kv + g) * nkv;
+    double *kd = malloc(sizeof(double) * (size_t)(nkv > 0 ? nkv : 1) * d);   /* k~ rows of the group */
+    double *dkd = calloc((size_t)(nkv > 0 ? nkv : 1) * d, sizeof(double));  /* dk~ */
+    double *bkd = calloc((size_t)(nkv > 0 ? nkv : 1) * d, sizeof(double));
+    double *vv = malloc(sizeof(double) * (size_t)(nkv > 0 ? nkv : 1) * dv);
+    double *s = malloc(sizeof(double) * (size_t)(nkv > 0 ? nkv : 1));
+    double *qd = malloc(sizeof(double) * d), *dqd = malloc(sizeof(double) * d), *bqd = malloc(sizeof(double) * d);
+    double *o = malloc(sizeof(double) * dv);
+    if (!kd || !dkd || !bkd || !vv || !s || !qd || !dqd || !bqd || !o) {
+        free(kd); free(dkd); free(bkd); free(vv); free(s); free(qd); free(dqd); free(bqd); free(o);
+        return ORACLE_INVALID_ARGUMENT;
+    }
+    for (int64_t j = 0; j < nkv; ++j) {
+        densify(J->k_idx, J->k_val, J->dtype, kvrow0 + j, k, d, kd + j * d);
+        for (int c = 0; c < dv; ++c) vv[j * dv + c] = widen(J->v, J->dtype, (kvrow0 + j) * dv + c);
+    }
+    double *dvg = J->dv + kvrow0 * dv; /* zero-initialised by the caller */
+    double *bvg = J->bv ? J->bv + kvrow0 * dv : NULL;
+    for (int r = 0; r < R; ++r) {
+        const int h = g * R + r;
+        for (int64_t i = 0; i < nq; ++i) {
+            const int64_t flat = ((int64_t)b * J->H + h) * nq + i;
+            int64_t jmax = nkv - 1;
+            if (J->causal && J->q_pos0 + i < jmax) jmax = J->q_pos0 + i; /* A9 */
+            for (int t = 0; t < k; ++t) {
+                J->dq[flat * k + t] = 0.0;
+                if (J->bq) J->bq[flat * k + t] = 0.0;
+            }
+            if (jmax < 0) continue; /* A10: no allowed key, no gradient */
+            densify(J->q_idx, J->q_val, J->dtype, flat, k, d, qd);
+            const double *dO = J->dO + flat * dv;
+            /* forward again: s, LSE, O (two passes, as ref_attn_fwd) */
+            double m = -INFINITY;
+            for (int64_t j = 0; j <= jmax; ++j) {
+                double acc = 0.0;
+                for (int u = 0; u < d; ++u) acc += qd[u] * kd[j * d + u];
+                s[j] = J->scale * acc;
+                if (s[j] > m) m = s[j];
+            }
+            double l = 0.0;
+            for (int64_t j = 0; j <= jmax; ++j) l += exp(s[j] - m);
+            const double lse = m + log(l);
+            for (int c = 0; c < dv; ++c) o[c] = 0.0;
+            for (int64_t j = 0; j <= jmax; ++j) {
+                const double p = exp(s[j] - lse);
+                for (int c = 0; c < dv; ++c) o[c] += p * vv[j * dv + c];
+            }
+            double D = 0.0, E = 0.0;
+            for (int c = 0; c < dv; ++c) {
+                D += dO[c] * o[c];
+                E += fabs(dO[c]) * (fabs(o[c]) + 1.0);
+            }
+            for (int u = 0; u < d; ++u) {
+                dqd[u] = 0.0;
+                bqd[u] = 0.0;
+            }
+            for (int64_t j = 0; j <= jmax; ++j) {
+                const double p = exp(s[j] - lse);
+                double dp = 0.0;
+                for (int c = 0; c < dv; ++c) dp += dO[c] * vv[j * dv + c];
+                const double ds = p * (dp - D);
+                const double w = p * (fabs(dp) + fabs(D) + E);
+                for (int c = 0; c < dv; ++c) {
+                    dvg[j * dv + c] += p * dO[c];
+                    if (bvg) bvg[j * dv + c] += p * fabs(dO[c]);
+                }
+                for (int u = 0; u < d; ++u) {
+                    dqd[u] += J->scale * ds * kd[j * d + u];
+                    bqd[u] += J->scale * w * fabs(kd[j * d + u]);
+                    dkd[j * d + u] += J->scale * ds * qd[u];
+                    bkd[j * d + u] += J->scale * w * fabs(qd[u]);
+                }
+            }
+            for (int t = 0; t < k; ++t) { /* Eq. topk_grad: the selected coordinates only */
+                const int u = J->q_idx[flat * k + t];
+                J->dq[flat * k + t] = dqd[u];
+                if (J->bq) J->bq[flat * k + t] = bqd[u];
+            }
+        }
+    }
+    for (int64_t j = 0; j < nkv; ++j)
+        for (int t = 0; t < k; ++t) {
+            const int u = J->k_idx[(kvrow0 + j) * k + t];
+            J->dk[(kvrow0 + j) * k + t] = dkd[j * d + u];
+            if (J->bk) J->bk[(kvrow0 + j) * k + t] = bkd[j * d + u];
+        }
+    free(kd); free(dkd); free(bkd); free(vv); free(s); free(qd); free(dqd); free(bqd); free(o);
+    return ORACLE_OK;
+}
+
+static void *bwd_worker(void *arg) {
+    bwd_job *J = (bwd_job *)arg;
+    for (;;) {
+        pthread_mutex_lock(&J->mu);
+        int64_t w = J->next++;
+        pthread_mutex_unlock(&J->mu);
+        if (w >= (int64_t)J->B * J->H_kv) break;
+        int st = bwd_group(J, (int)(w / J->H_kv), (int)(w % J->H_kv));
+        if (st) {
+            pthread_mutex_lock(&J->mu);
+            J->status = st;
+            pthread_mutex_unlock(&J->mu);
+        }
+    }
+    return NULL;
+}
+
+int ref_attn_bwd(int B, int H, int H_kv, int d, int k, int d_v, int64_t n_q, int64_t n_kv, int64_t q_pos0,
+                 int causal, double scale, int dtype, const uint8_t *q_idx, const void *q_val, const uint8_t *k_idx,
+                 const void *k_val, const void *v, const double *dO, double *dq, double *dk, double *dv, double *bq,
+                 double *bk, double *bv, int threads) {
+    if (B < 1 || H < 1 || H_kv < 1 || H % H_kv || d < 1 || d > 256 || k < 1 || k > d || d_v < 1 || n_q < 0 ||
+        n_kv < 0 || dtype < 0 || dtype > 2 || !(scale > 0) || !isfinite(scale))
+        return ORACLE_INVALID_ARGUMENT;
+    bwd_job J;
+    memset(&J, 0, sizeof J);
+    J.B = B; J.H = H; J.H_kv = H_kv; J.d = d; J.k = k; J.d_v = d_v; J.causal = causal; J.dtype = dtype;
+    J.n_q = n_q; J.n_kv = n_kv; J.q_pos0 = q_pos0; J.scale = scale;
+    J.q_idx = q_idx; J.k_idx = k_idx; J.q_val = q_val; J.k_val = k_val; J.v = v; J.dO = dO;
+    J.dq = dq; J.dk = dk; J.dv = dv; J.bq = bq; J.bk = bk; J.bv = bv;
+    memset(dv, 0, sizeof(double) * (size_t)B * H_kv * n_kv * d_v);
+    if (bv) memset(bv, 0, sizeof(double) * (size_t)B * H_kv * n_kv * d_v);
+    pthread_mutex_init(&J.mu, NULL);
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    pthread_t tid[256];
+    for (int t = 0; t < threads; ++t) pthread_create(&tid[t], NULL, bwd_worker, &J);
+    for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+    pthread_mutex_destroy(&J.mu);
+    return J.status;
 }
