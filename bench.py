@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--k", type=int, default=None, help="override the code size k (sweep)")
-    ap.add_argument("--mode", default="forward", choices=["forward", "decode"],
+    ap.add_argument("--mode", default="forward", choices=["forward", "decode", "bwd"],
                     help="decode: SURVEY 8(f) N2, one new query row per sequence over a cached K/V of the config's n")
     ap.add_argument("--decode-batch", type=int, default=8, help="sequences per GPU in --mode decode")
     ap.add_argument("--shard-seq", action="store_true",
@@ -192,6 +192,88 @@ L2_FLUSH_MB = 512
 
 
 # --------------------------------------------------------------------------------------------
+def run_bwd(args, W, rank, world, local):
+    """the backward with the straight-through rule (sfa_attn_bwd) on the metric's
+    workload.  Inputs: codes of generated Q/K, V, the forward's O/LSE, a generated upstream dO.  The
+    step is the D prep + the dK~/dV and dQ~ tensor-core kernels (P recomputed from the codes)."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_22300_b200 import inputs, sfa
+    dev = torch.device("cuda", local)
+    B, H, H_kv, n, d, d_v, k = W.B, W.H, W.H_kv, W.n, W.d, W.d_v, W.k
+    seed = accounting.SEEDS[args.config]
+    bf = torch.bfloat16
+    Q = sfa.gen_fill(torch.empty((B, H, n, d), dtype=bf, device=dev), seed, inputs.TID_Q, offset=rank * B * H * n * d)
+    K = sfa.gen_fill(torch.empty((B, H_kv, n, d), dtype=bf, device=dev), seed, inputs.TID_K, offset=rank * B * H_kv * n * d)
+    V = sfa.gen_fill(torch.empty((B, H_kv, n, d_v), dtype=bf, device=dev), seed, inputs.TID_V,
+                     offset=rank * B * H_kv * n * d_v)
+    dO = sfa.gen_fill(torch.empty((B, H, n, d_v), dtype=bf, device=dev), seed, inputs.TID_DO,
+                      offset=rank * B * H * n * d_v)
+    qi, qv = sfa.topk_codes(Q, k)
+    ki, kv = sfa.topk_codes(K, k)
+    del Q, K
+    O, LSE = sfa.attn_fwd(qi, qv, ki, kv, V, d=d, causal=W.causal)
+    f32 = dict(dtype=torch.float32, device=dev)
+    dq, dk, dv = (torch.empty((B, H, n, k), **f32), torch.empty((B, H_kv, n, k), **f32),
+                  torch.empty((B, H_kv, n, d_v), **f32))
+    desc = sfa.make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k, d_v=d_v, n_q=n, n_kv=n, causal=W.causal)
+    L = sfa.lib()
+    ws = torch.empty(max(int(L.sfa_attn_bwd_workspace_bytes(ctypes.byref(desc))), 16), dtype=torch.uint8, device=dev)
+    flush = torch.empty(L2_FLUSH_MB * 2 ** 20, dtype=torch.uint8, device=dev)
+    P_ = lambda t: ctypes.c_void_p(t.data_ptr())
+    st = lambda: ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def step():
+        r = L.sfa_attn_bwd(ctypes.byref(desc), P_(qi), P_(qv), P_(ki), P_(kv), P_(V), P_(O), P_(LSE), P_(dO), P_(dq),
+                           P_(dk), P_(dv), P_(ws), ws.numel(), st())
+        if r:
+            raise RuntimeError(f"sfa_attn_bwd failed: {r}")
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for e0, e1 in evs:
+            flush.zero_()
+            e0.record()
+            step()
+            e1.record()
+        torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    pk = peaks()
+    pairs = B * H * accounting.causal_pairs(n, n, 0, W.causal)
+    # tensor FLOPs per allowed pair: S and dP recomputed in both kernels (2 x (2d + 2d_v)), then
+    # dV (2 d_v), dK~ (2 d) and dQ~ (2 d)
+    flops = pairs * (8 * d + 6 * d_v)
+    tf = flops / (ms / 1e3) / 1e12
+    if rank == 0:
+        line = {"metric": "FlashSFA backward (straight-through rule) ms & tokens/s at n=32K, d=128, k=16 (SURVEY 8(f) N1)",
+                "value": B * n * world / (ms / 1e3), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded generator; codes from sfa_topk_codes)",
+                "config": {"workload": f"{args.config} backward: B={B} per GPU, H={H}, H_kv={H_kv}, n={n}, d={d}, "
+                                       f"d_v={d_v}, k={k}, causal", "global_batch": B * world, "seq_len": n,
+                           "parallelism": "weak: batch element r on rank r", "l2": f"explicit {L2_FLUSH_MB} MB write between steps"},
+                "roofline": {"bound": "tensor", "kernel": "bwd_dkdv_kernel + bwd_dq_kernel",
+                             "achieved": tf, "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": tf / pk["bf16_tflops"],
+                             "traffic": None, "flops_per_pair": 8 * d + 6 * d_v,
+                             "mufu_floor_ms": 2 * pairs / (N_SMS * MUFU_EX2_PER_CLK_SM * pk["sm_max_mhz"] * 1e6) * 1e3},
+                "cpu_baseline": None, "e2e": None, "gpu_launches": 3 * args.steps, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+
+
 def run_decode(args, W, rank, world, local):
     """a decode step -- one query row per (sequence, head) against a K/V cache of n
     tokens already coded (k-sparse key codes + bf16 V in HBM).  HBM-bound: the algorithmic traffic is
@@ -399,6 +481,13 @@ def main():
 
     from paper_2603_22300_b200 import inputs, sfa
     torch.cuda.set_device(local)
+    if args.mode == "bwd":
+        if world > 1 and not dist.is_initialized():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        run_bwd(args, W, rank, world, local)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     if args.mode == "decode":
         if world > 1 and not dist.is_initialized():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))

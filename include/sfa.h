@@ -133,6 +133,26 @@ SFA_API sfa_status sfa_attn_fwd_prepared(const sfa_attn_desc *desc, const uint8_
                                          const uint8_t *k_idx, const void *k_val, const void *v, void *o, float *lse,
                                          const void *workspace, size_t workspace_bytes, sfa_stream_t stream);
 
+/* ------------------------------------------------------------------------------------------
+ * Backward: the straight-through rule of P:L103-112 (Sec. 3.1 "Backward
+ * computation", Eq. topk_grad) composed with the softmax-attention backward.
+ *   Inputs: the forward's codes, v, o and lse (same desc; bf16 only) and the upstream gradient
+ *   dO [B][H][n_q][d_v] bf16.  Outputs (fp32, device, caller-owned, fully overwritten):
+ *     dq_val [B][H][n_q][k]     = dL/dq~ at the selected coordinates q_idx (the dense dQ of
+ *                                 Eq. topk_grad is this scattered to the support, 0 elsewhere)
+ *     dk_val [B][H_kv][n_kv][k] = dL/dk~ at k_idx, summed over the kv head's query heads
+ *     dv     [B][H_kv][n_kv][d_v]
+ *   workspace >= sfa_attn_bwd_workspace_bytes(desc) (D_i = rowsum(dO . O), fp32 per query row).
+ *   P is recomputed from the codes and lse (never stored); P and dS enter the tensor cores in
+ *   bf16 (reading A24).  Deterministic: no atomics, fixed reduction order.
+ *   Errors: fp32 desc or d, d_v not in {64, 128} -> SFA_ERR_UNSUPPORTED; null / misaligned
+ *   pointers -> SFA_ERR_INVALID_ARGUMENT; short workspace -> SFA_ERR_RESOURCE. */
+SFA_API size_t sfa_attn_bwd_workspace_bytes(const sfa_attn_desc *desc);
+SFA_API sfa_status sfa_attn_bwd(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val,
+                                const uint8_t *k_idx, const void *k_val, const void *v, const void *o,
+                                const float *lse, const void *dO, float *dq_val, float *dk_val, float *dv,
+                                void *workspace, size_t workspace_bytes, sfa_stream_t stream);
+
 /* SIMT only -- step 3 alone (exposed for the bucket-layout tests):
  * builds the buckets of every key tile into `workspace` (layout in DESIGN.md).  sfa_attn_fwd calls it. */
 SFA_API sfa_status sfa_bucket_keys(const sfa_attn_desc *desc, const uint8_t *k_idx, const void *k_val, void *workspace,

@@ -252,6 +252,31 @@ sfa_status sfa_attn_fwd_prepared(const sfa_attn_desc *desc, const uint8_t *q_idx
     return run_attn_prepared(desc, q_idx, q_val, k_idx, k_val, v, o, lse, (void *)workspace, (cudaStream_t)stream);
 }
 
+size_t sfa_attn_bwd_workspace_bytes(const sfa_attn_desc *desc) {
+    if (validate_desc(desc) != SFA_OK) return 0;
+    return (size_t)desc->B * desc->H * desc->n_q * sizeof(float);
+}
+
+sfa_status sfa_attn_bwd(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val, const uint8_t *k_idx,
+                        const void *k_val, const void *v, const void *o, const float *lse, const void *dO,
+                        float *dq_val, float *dk_val, float *dv, void *workspace, size_t workspace_bytes,
+                        sfa_stream_t stream) {
+    sfa_status s = validate_desc(desc);
+    if (s != SFA_OK) return s;
+    if (desc->dtype != SFA_BF16) return SFA_ERR_UNSUPPORTED;
+    if (!q_idx || !q_val || !k_idx || !k_val || !v || !o || !lse || !dO || !dq_val || !dk_val || !dv || !workspace)
+        return SFA_ERR_INVALID_ARGUMENT;
+    if (!aligned16(v) || !aligned16(o) || !aligned16(dO) || !aligned16(dv) || !aligned16(workspace) ||
+        ((uintptr_t)lse & 3u) || ((uintptr_t)dq_val & 3u) || ((uintptr_t)dk_val & 3u) ||
+        !codes_aligned(q_idx, q_val) || !codes_aligned(k_idx, k_val))
+        return SFA_ERR_INVALID_ARGUMENT;
+    if (workspace_bytes < sfa_attn_bwd_workspace_bytes(desc)) return SFA_ERR_RESOURCE;
+    const AttnParams p = make_params(desc, q_idx, q_val, k_idx, k_val, v, const_cast<void *>(o),
+                                     const_cast<float *>(lse), workspace);
+    return from_launch(launch_attn_bwd(p, desc->d, desc->d_v, dO, static_cast<float *>(workspace), dq_val, dk_val, dv,
+                                       (cudaStream_t)stream));
+}
+
 sfa_status sfa_debug_sm100_scores(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val,
                                   const uint8_t *k_idx, const void *k_val, const void *v, void *o, float *lse,
                                   void *workspace, size_t workspace_bytes, float *scores, sfa_stream_t stream) {

@@ -1,0 +1,596 @@
+// bwd.cu -- FlashSFA backward with the straight-through rule on sm_100a tensor cores
+// (Sec. 3.1 "Backward computation", Eq. topk_grad).
+//
+// With P_ij = exp(s_ij - LSE_i) recomputed from the codes and the forward's LSE, and
+// D_i = sum_c dO_ic O_ic:
+//   dP = dO V^T,  dS = P (.) (dP - D),  dV = P^T dO,  dQ~ = scale dS K~,  dK~ = scale dS^T Q~,
+// and the straight-through rule keeps only the selected coordinates: dq_val[i][t] = dQ~[i][q_idx[i][t]],
+// dk_val[j][t] = dK~[j][k_idx[j][t]] (the dense dQ, dK of Eq. topk_grad are these scattered to the
+// supports, zero elsewhere).  GQA: dK~ and dV of a kv head sum over its query heads (A15).
+//
+// Two kernels, no atomics, every reduction in a fixed order (S "Concurrency Model": deterministic):
+//   bwd_dq_kernel    one CTA per 128-row query tile (query-stationary, like the forward):
+//                    per key tile S = Q~ K~^T and dP = dO V^T (SS-MMAs, M = 128 queries), the row
+//                    warps form dS in bf16 into S's TMEM columns, dQ~ += dS K~ (TS-MMA, K~ read
+//                    MN-major from the same swizzled tile);
+//   bwd_dkdv_kernel  one CTA per 128-key tile of a kv head (key-stationary): per (query head of the
+//                    group, query tile) S^T = K~ Q~^T and dP^T = V dO^T (M = 128 keys), the key
+//                    warps form P^T and dS^T in bf16 in TMEM, dV += P^T dO and dK~ += dS^T Q~
+//                    (TS-MMAs, dO and Q~ read MN-major).
+// Both recompute the scores exactly as the forward (bf16 products are exact in fp32); P and dS are
+// rounded to bf16 for the tensor cores (reading A24: the gradient tolerance is componentwise).
+// Operands: codes decompressed on chip into 128B-swizzled tiles (densify.cuh), V and dO by TMA.
+#include <cudaTypedefs.h>
+#include <mutex>
+
+#include "densify.cuh"
+#include "launch.cuh"
+#include "sm100.cuh"
+
+namespace sfa {
+using namespace sm100;
+using namespace dz;
+
+namespace {
+
+constexpr int BM = 128, BN = 128, NTH = 384;
+
+struct BwdArgs {
+    const uint8_t *q_idx, *k_idx;
+    const uint16_t *q_val, *k_val;
+    const float *lse, *Dr;  // [B][H][n_q]: forward LSE, D_i = rowsum(dO . O)
+    float *dq, *dk, *dv;    // [B][H][n_q][k], [B][H_kv][n_kv][k], [B][H_kv][n_kv][d_v] (fp32)
+    int32_t B, H, H_kv, k;
+    int64_t n_q, n_kv, q_pos0;
+    int32_t causal, nqb, nkt;
+    float scale, c_scale;  // scale, scale * log2(e)
+};
+
+__global__ void bwd_prep_kernel(const uint16_t *__restrict__ o, const uint16_t *__restrict__ dO, int64_t rows,
+                                int d_v, float *__restrict__ Dr) {
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    float acc = 0.f;
+    for (int c = lane; c < d_v; c += 32) {
+        const float a = __uint_as_float((uint32_t)__ldg(o + row * d_v + c) << 16);
+        const float b = __uint_as_float((uint32_t)__ldg(dO + row * d_v + c) << 16);
+        acc = fmaf(a, b, acc);
+    }
+#pragma unroll
+    for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+    if (lane == 0) Dr[row] = acc;
+}
+
+// SW128 operand descriptors: K-major tile of `rows` rows, K-step kk (16 elements); MN-major view of
+// the same tile (rows = the K dimension), K-step kk = 16 rows
+__device__ __forceinline__ uint64_t kmaj(uint32_t base, int rows, int kk) {
+    return umma_desc_sw128(base + (uint32_t)((kk >> 2) * rows * 128 + (kk & 3) * 32), 16, 1024);
+}
+__device__ __forceinline__ uint64_t mnmaj(uint32_t base, int rows, int kk) {
+    return umma_desc_sw128(base + (uint32_t)(kk * 2048), (uint32_t)rows * 128, 1024);
+}
+
+// ---------------------------------------------------------------------------------------------
+// dQ: one CTA per (b, h, query tile)
+// ---------------------------------------------------------------------------------------------
+template <int D, int DV>
+struct DqCfg {
+    static constexpr int OFF_Q = 0;                      // Q~ tile  [128][D] bf16
+    static constexpr int OFF_DO = OFF_Q + BM * D * 2;    // dO tile  [128][DV] bf16
+    static constexpr int OFF_K = OFF_DO + BM * DV * 2;   // K~ ring  2 x [128][D]
+    static constexpr int OFF_V = OFF_K + 2 * BN * D * 2; // V ring   2 x [128][DV]
+    static constexpr int OFF_BAR = OFF_V + 2 * BN * DV * 2;
+    static constexpr int SMEM = OFF_BAR + 256 + 1024;
+};
+enum { Q_FULL = 0, DO_FULL, K_FULL, K_EMPTY = K_FULL + 2, V_FULL = K_EMPTY + 2, V_EMPTY = V_FULL + 2, S_FULL = V_EMPTY + 2,
+       DS_READY, DQ_FULL, NBAR_DQ };
+
+template <int D, int DV>
+__global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_v,
+                                                        const __grid_constant__ CUtensorMap tm_do, const BwdArgs a) {
+    using C = DqCfg<D, DV>;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_s = smem_u32(smem_raw);
+    const uint32_t sb = (raw_s + 1023u) & ~1023u;
+    uint8_t *gb = smem_raw + (sb - raw_s);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#define BAR(i) (sb + C::OFF_BAR + 8u * (uint32_t)(i))
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gb + C::OFF_BAR + 200);
+
+    const int bh_n = a.B * a.H;
+    const int ib = a.nqb - 1 - (int)(blockIdx.x / bh_n);  // heaviest causal tiles first
+    const int bh = (int)(blockIdx.x % bh_n), b = bh / a.H, h = bh % a.H, g = h / (a.H / a.H_kv);
+    int nt = a.nkt;
+    if (a.causal) {
+        int64_t last = (int64_t)ib * BM + BM - 1;
+        if (last > a.n_q - 1) last = a.n_q - 1;
+        const int64_t lim = (a.q_pos0 + last) / BN + 1;
+        if (lim < nt) nt = (int)lim;
+    }
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NBAR_DQ; ++i)
+            mbar_init(BAR(i), (i == Q_FULL || i == K_FULL || i == K_FULL + 1 || i == DS_READY) ? 4u : 1u);
+        fence_mbar_init();
+    }
+    if (warp == 8) tmem_alloc<512>(smem_u32(tmem_slot));
+    if (warp == 9 && lane == 0) {
+        tma_prefetch_desc(&tm_v);
+        tma_prefetch_desc(&tm_do);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < 4) {
+        // ==================== row warps: thread = query row = TMEM lane ====================
+        const int r = warp * 32 + lane;
+        const uint32_t lo = (uint32_t)(warp * 32) << 16;
+        const int64_t i = (int64_t)ib * BM + r;
+        const bool row_ok = i < a.n_q;
+        const int64_t qrow = ((int64_t)b * a.H + h) * a.n_q + i;
+        const float lse2 = row_ok ? __ldg(a.lse + qrow) * 1.4426950408889634f : 0.f;
+        const float Di = row_ok ? __ldg(a.Dr + qrow) : 0.f;
+        int64_t kend = row_ok ? a.n_kv : 0;
+        if (row_ok && a.causal && a.q_pos0 + i + 1 < kend) kend = a.q_pos0 + i + 1;
+        const float cs = a.c_scale;
+        for (int j = 0; j < nt; ++j) {
+            mbar_wait(BAR(S_FULL), j & 1);
+            tc_fence_after();
+            int64_t l64 = kend - (int64_t)j * BN;
+            const int lim = l64 < 0 ? 0 : (l64 > BN ? BN : (int)l64);
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {  // 32 keys at a time; dS(c) overwrites S columns already read
+                uint32_t s[32], dp[32], pk[16];
+                tmem_ld32(tmem + lo + 32 * c, s);
+                tmem_ld32(tmem + lo + 128 + 32 * c, dp);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const int k0 = 32 * c + 2 * e;
+                    const float p0 = k0 < lim ? fast_exp2(fmaf(__uint_as_float(s[2 * e]), cs, -lse2)) : 0.f;
+                    const float p1 = k0 + 1 < lim ? fast_exp2(fmaf(__uint_as_float(s[2 * e + 1]), cs, -lse2)) : 0.f;
+                    pk[e] = pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - Di), p1 * (__uint_as_float(dp[2 * e + 1]) - Di));
+                }
+                tmem_st16(tmem + lo + 16 * c, pk);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(BAR(DS_READY));
+        }
+        // ---- epilogue: dQ~ row -> shared staging (the dead K~ ring) -> gather at the support
+        mbar_wait(BAR(DQ_FULL), 0);
+        tc_fence_after();
+        float *st = reinterpret_cast<float *>(gb + C::OFF_K) + (size_t)r * D;
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tmem + lo + 256 + 32 * c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) st[(32 * c + e + r) % D] = __uint_as_float(o[e]);  // rotated: no bank conflicts
+        }
+        if (row_ok)
+            for (int t = 0; t < a.k; ++t) {
+                const int f = __ldg(a.q_idx + qrow * a.k + t);
+                a.dq[qrow * a.k + t] = a.scale * st[(f + r) % D];
+            }
+    } else if (warp < 8) {
+        // ==================== decompression: Q~ once, K~ per key tile (thread = row) ====================
+        const int r = threadIdx.x - 128;
+        const int k = a.k;
+        {
+            const int64_t i = (int64_t)ib * BM + r;
+            const bool ok = i < a.n_q;
+            const int64_t row = ((int64_t)b * a.H + h) * a.n_q + (ok ? i : 0);
+            densify_row<D>(sb + C::OFF_Q, BM, r, ok, a.q_idx + row * k, a.q_val + row * k, k);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(Q_FULL));
+        const int64_t kv0 = ((int64_t)b * a.H_kv + g) * a.n_kv;
+        for (int j = 0; j < nt; ++j) {
+            const int s = j & 1, u = j >> 1;
+            const int64_t key = (int64_t)j * BN + r;
+            const bool ok = key < a.n_kv;
+            const int64_t kr = kv0 + (ok ? key : 0);
+            mbar_wait(BAR(K_EMPTY + s), (u & 1) ^ 1);
+            densify_row<D>(sb + C::OFF_K + s * BN * D * 2, BN, r, ok, a.k_idx + kr * k, a.k_val + kr * k, k);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(BAR(K_FULL + s));
+        }
+    } else if (warp == 8) {
+        // ==================== tcgen05.mma issuer ====================
+        if (lane == 0) {
+            constexpr uint32_t idS = umma_idesc_f16kind(BM, BN, 0, 0, 1);  // Q~ . K~^T
+            constexpr uint32_t idQ = umma_idesc_f16kind(BM, D, 0, 1, 1);   // dS[TMEM] . K~ (K~ MN-major)
+            const uint32_t qa = sb + C::OFF_Q, da = sb + C::OFF_DO;
+            mbar_wait(BAR(Q_FULL), 0);
+            mbar_wait(BAR(DO_FULL), 0);
+            auto dq_mma = [&](int jj) {  // dQ~ += dS(jj) K~(jj)
+                mbar_wait(BAR(DS_READY), jj & 1);
+                tc_fence_after();
+                const uint32_t ka = sb + C::OFF_K + (jj & 1) * BN * D * 2;
+#pragma unroll
+                for (int kk = 0; kk < BN / 16; ++kk)
+                    umma_ts(tmem + 256, tmem + 8 * kk, mnmaj(ka, BN, kk), idQ, (jj > 0 || kk > 0) ? 1u : 0u);
+                umma_commit(BAR(K_EMPTY + (jj & 1)));
+            };
+            for (int j = 0; j < nt; ++j) {
+                const int s = j & 1, u = j >> 1;
+                mbar_wait(BAR(K_FULL + s), u & 1);
+                mbar_wait(BAR(V_FULL + s), u & 1);
+                tc_fence_after();
+                if (j > 0) dq_mma(j - 1);  // in-order pipe: reads dS(j-1) before S(j) overwrites it
+                const uint32_t ka = sb + C::OFF_K + s * BN * D * 2, va = sb + C::OFF_V + s * BN * DV * 2;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) umma_ss(tmem, kmaj(qa, BM, kk), kmaj(ka, BN, kk), idS, kk > 0);
+#pragma unroll
+                for (int kk = 0; kk < DV / 16; ++kk)
+                    umma_ss(tmem + 128, kmaj(da, BM, kk), kmaj(va, BN, kk), idS, kk > 0);
+                umma_commit(BAR(V_EMPTY + s));
+                umma_commit(BAR(S_FULL));
+            }
+            dq_mma(nt - 1);
+            umma_commit(BAR(DQ_FULL));
+        }
+        __syncwarp();
+    } else if (warp == 9) {
+        // ==================== TMA: dO tile once, V tiles ====================
+        if (lane == 0) {
+            mbar_arrive_expect_tx(BAR(DO_FULL), BM * DV * 2);
+#pragma unroll
+            for (int cb = 0; cb < DV / 64; ++cb)
+                tma_load_3d(sb + C::OFF_DO + cb * BM * 128, &tm_do, BAR(DO_FULL), cb * 64, ib * BM, b * a.H + h);
+            for (int j = 0; j < nt; ++j) {
+                const int s = j & 1, u = j >> 1;
+                mbar_wait(BAR(V_EMPTY + s), (u & 1) ^ 1);
+                mbar_arrive_expect_tx(BAR(V_FULL + s), BN * DV * 2);
+#pragma unroll
+                for (int cb = 0; cb < DV / 64; ++cb)
+                    tma_load_3d(sb + C::OFF_V + s * BN * DV * 2 + cb * BN * 128, &tm_v, BAR(V_FULL + s), cb * 64,
+                                j * BN, b * a.H_kv + g);
+            }
+        }
+        __syncwarp();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 8) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+#undef BAR
+}
+
+// ---------------------------------------------------------------------------------------------
+// dK, dV: one CTA per (b, kv head, key tile)
+// ---------------------------------------------------------------------------------------------
+template <int D, int DV>
+struct KvCfg {
+    static constexpr int OFF_K = 0;                        // K~ tile [128][D]
+    static constexpr int OFF_V = OFF_K + BN * D * 2;       // V tile  [128][DV]
+    static constexpr int OFF_Q = OFF_V + BN * DV * 2;      // Q~ ring 2 x [128][D]
+    static constexpr int OFF_DO = OFF_Q + 2 * BM * D * 2;  // dO ring 2 x [128][DV]
+    static constexpr int OFF_LD = OFF_DO + 2 * BM * DV * 2; // 2 stages x {LSE*log2e, D} x 128 fp32
+    static constexpr int OFF_BAR = OFF_LD + 2 * 2 * BM * 4;
+    static constexpr int SMEM = OFF_BAR + 256 + 1024;
+};
+enum { KK_FULL = 0, KV_FULL, QQ_FULL, QQ_EMPTY = QQ_FULL + 2, DOO_FULL = QQ_EMPTY + 2, DOO_EMPTY = DOO_FULL + 2,
+       SS_FULL = DOO_EMPTY + 2, P_READY, OUT_FULL, NBAR_KV };
+
+template <int D, int DV>
+__global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_v,
+                                                          const __grid_constant__ CUtensorMap tm_do, const BwdArgs a) {
+    using C = KvCfg<D, DV>;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_s = smem_u32(smem_raw);
+    const uint32_t sb = (raw_s + 1023u) & ~1023u;
+    uint8_t *gb = smem_raw + (sb - raw_s);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#define BAR(i) (sb + C::OFF_BAR + 8u * (uint32_t)(i))
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gb + C::OFF_BAR + 200);
+    float *ldv = reinterpret_cast<float *>(gb + C::OFF_LD);  // [stage][{lse2, D}][128]
+
+    const int bg_n = a.B * a.H_kv;
+    const int jb = (int)(blockIdx.x / bg_n);  // low key tiles see the most query tiles: first
+    const int bg = (int)(blockIdx.x % bg_n), b = bg / a.H_kv, g = bg % a.H_kv;
+    const int R = a.H / a.H_kv;
+    int ib0 = 0;
+    if (a.causal) {  // first query tile holding a query at or after this tile's first key
+        const int64_t first = (int64_t)jb * BN - a.q_pos0;
+        ib0 = first <= 0 ? 0 : (int)(first / BM);
+    }
+    const int nib = a.nqb > ib0 ? a.nqb - ib0 : 0;
+    const int ns = R * nib;  // steps: (query head of the group, query tile)
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NBAR_KV; ++i)
+            mbar_init(BAR(i), (i == KK_FULL || i == QQ_FULL || i == QQ_FULL + 1 || i == P_READY) ? 4u : 1u);
+        fence_mbar_init();
+    }
+    if (warp == 8) tmem_alloc<512>(smem_u32(tmem_slot));
+    if (warp == 9 && lane == 0) {
+        tma_prefetch_desc(&tm_v);
+        tma_prefetch_desc(&tm_do);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    constexpr uint32_t DV_COL = 256, DK_COL = 256 + DV;
+
+    if (warp < 4) {
+        // ==================== key warps: thread = key = TMEM lane ====================
+        const int r = warp * 32 + lane;
+        const uint32_t lo = (uint32_t)(warp * 32) << 16;
+        const int64_t kj = (int64_t)jb * BN + r;
+        const bool key_ok = kj < a.n_kv;
+        const float cs = a.c_scale;
+        for (int s = 0; s < ns; ++s) {
+            const int st = s & 1, ib = ib0 + s % nib;
+            mbar_wait(BAR(SS_FULL), s & 1);
+            mbar_wait(BAR(QQ_FULL + st), (s >> 1) & 1);  // LSE / D of this step visible (generic stores)
+            tc_fence_after();
+            const float *lse2 = ldv + st * 2 * BM, *Dq = lse2 + BM;
+            // query q of this tile may use key kj iff q < n_q and (non-causal or kj <= q_pos0 + q)
+            int64_t qmin = a.causal ? kj - a.q_pos0 - (int64_t)ib * BM : 0;  // first allowed local query
+            if (qmin < 0) qmin = 0;
+            int64_t qmax = a.n_q - (int64_t)ib * BM;                          // one past the last valid
+            if (!key_ok) qmax = 0;
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                uint32_t sv[32], dp[32], pp[16], pd[16];
+                tmem_ld32(tmem + lo + 32 * c, sv);
+                tmem_ld32(tmem + lo + 128 + 32 * c, dp);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                    const int q0 = 32 * c + 2 * e;
+                    const bool a0 = q0 >= qmin && q0 < qmax, a1 = q0 + 1 >= qmin && q0 + 1 < qmax;
+                    const float p0 = a0 ? fast_exp2(fmaf(__uint_as_float(sv[2 * e]), cs, -lse2[q0])) : 0.f;
+                    const float p1 = a1 ? fast_exp2(fmaf(__uint_as_float(sv[2 * e + 1]), cs, -lse2[q0 + 1])) : 0.f;
+                    pp[e] = pack_bf16x2(p0, p1);
+                    pd[e] = pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - Dq[q0]),
+                                        p1 * (__uint_as_float(dp[2 * e + 1]) - Dq[q0 + 1]));
+                }
+                tmem_st16(tmem + lo + 16 * c, pp);        // P^T over S^T's columns already read
+                tmem_st16(tmem + lo + 128 + 16 * c, pd);  // dS^T over dP^T's
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(BAR(P_READY));
+        }
+        // ---- epilogue: dV row (fp32) straight out; dK~ row -> staging (dead Q~ ring) -> support gather
+        const int64_t krow = ((int64_t)b * a.H_kv + g) * a.n_kv + kj;
+        float *stg = reinterpret_cast<float *>(gb + C::OFF_Q) + (size_t)r * D;
+        if (ns > 0) {
+            mbar_wait(BAR(OUT_FULL), 0);
+            tc_fence_after();
+        }
+#pragma unroll 1
+        for (int c = 0; c < DV / 32; ++c) {
+            uint32_t o[32];
+            if (ns > 0) {
+                tmem_ld32(tmem + lo + DV_COL + 32 * c, o);
+                tmem_ld_wait();
+            } else {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) o[e] = 0u;
+            }
+            if (key_ok) {
+                float4 *dst = reinterpret_cast<float4 *>(a.dv + krow * DV + 32 * c);
+#pragma unroll
+                for (int v4 = 0; v4 < 8; ++v4)
+                    dst[v4] = make_float4(__uint_as_float(o[4 * v4]), __uint_as_float(o[4 * v4 + 1]),
+                                          __uint_as_float(o[4 * v4 + 2]), __uint_as_float(o[4 * v4 + 3]));
+            }
+        }
+#pragma unroll 1
+        for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            if (ns > 0) {
+                tmem_ld32(tmem + lo + DK_COL + 32 * c, o);
+                tmem_ld_wait();
+            } else {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) o[e] = 0u;
+            }
+#pragma unroll
+            for (int e = 0; e < 32; ++e) stg[(32 * c + e + r) % D] = __uint_as_float(o[e]);
+        }
+        if (key_ok)
+            for (int t = 0; t < a.k; ++t) {
+                const int f = __ldg(a.k_idx + krow * a.k + t);
+                a.dk[krow * a.k + t] = a.scale * stg[(f + r) % D];
+            }
+    } else if (warp < 8) {
+        // ==================== decompression: K~ once, Q~ (+ LSE, D) per step (thread = row) ====================
+        const int r = threadIdx.x - 128;
+        const int k = a.k;
+        const int64_t kv0 = ((int64_t)b * a.H_kv + g) * a.n_kv;
+        {
+            const int64_t key = (int64_t)jb * BN + r;
+            const bool ok = key < a.n_kv;
+            const int64_t kr = kv0 + (ok ? key : 0);
+            densify_row<D>(sb + C::OFF_K, BN, r, ok, a.k_idx + kr * k, a.k_val + kr * k, k);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(KK_FULL));
+        for (int s = 0; s < ns; ++s) {
+            const int st = s & 1, u = s >> 1;
+            const int h = g * R + s / nib, ib = ib0 + s % nib;
+            const int64_t i = (int64_t)ib * BM + r;
+            const bool ok = i < a.n_q;
+            const int64_t row = ((int64_t)b * a.H + h) * a.n_q + (ok ? i : 0);
+            mbar_wait(BAR(QQ_EMPTY + st), (u & 1) ^ 1);
+            densify_row<D>(sb + C::OFF_Q + st * BM * D * 2, BM, r, ok, a.q_idx + row * k, a.q_val + row * k, k);
+            ldv[st * 2 * BM + r] = ok ? __ldg(a.lse + row) * 1.4426950408889634f : 0.f;
+            ldv[st * 2 * BM + BM + r] = ok ? __ldg(a.Dr + row) : 0.f;
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(BAR(QQ_FULL + st));
+        }
+    } else if (warp == 8) {
+        // ==================== tcgen05.mma issuer ====================
+        if (lane == 0 && ns > 0) {
+            constexpr uint32_t idS = umma_idesc_f16kind(BN, BM, 0, 0, 1);  // K~ . Q~^T and V . dO^T
+            constexpr uint32_t idV = umma_idesc_f16kind(BN, DV, 0, 1, 1);  // P^T[TMEM] . dO (MN-major)
+            constexpr uint32_t idK = umma_idesc_f16kind(BN, D, 0, 1, 1);   // dS^T[TMEM] . Q~ (MN-major)
+            const uint32_t ka = sb + C::OFF_K, va = sb + C::OFF_V;
+            mbar_wait(BAR(KK_FULL), 0);
+            mbar_wait(BAR(KV_FULL), 0);
+            auto grad_mma = [&](int ss) {  // dV += P^T(ss) dO(ss), dK~ += dS^T(ss) Q~(ss)
+                const int st = ss & 1;
+                mbar_wait(BAR(P_READY), ss & 1);
+                tc_fence_after();
+                const uint32_t qa = sb + C::OFF_Q + st * BM * D * 2, da = sb + C::OFF_DO + st * BM * DV * 2;
+#pragma unroll
+                for (int kk = 0; kk < BM / 16; ++kk)
+                    umma_ts(tmem + DV_COL, tmem + 8 * kk, mnmaj(da, BM, kk), idV, (ss > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+                for (int kk = 0; kk < BM / 16; ++kk)
+                    umma_ts(tmem + DK_COL, tmem + 128 + 8 * kk, mnmaj(qa, BM, kk), idK, (ss > 0 || kk > 0) ? 1u : 0u);
+                umma_commit(BAR(QQ_EMPTY + st));
+                umma_commit(BAR(DOO_EMPTY + st));
+            };
+            for (int s = 0; s < ns; ++s) {
+                const int st = s & 1, u = s >> 1;
+                mbar_wait(BAR(QQ_FULL + st), u & 1);
+                mbar_wait(BAR(DOO_FULL + st), u & 1);
+                tc_fence_after();
+                if (s > 0) grad_mma(s - 1);  // in-order pipe: reads P^T/dS^T(s-1) before S^T(s) lands
+                const uint32_t qa = sb + C::OFF_Q + st * BM * D * 2, da = sb + C::OFF_DO + st * BM * DV * 2;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) umma_ss(tmem, kmaj(ka, BN, kk), kmaj(qa, BM, kk), idS, kk > 0);
+#pragma unroll
+                for (int kk = 0; kk < DV / 16; ++kk)
+                    umma_ss(tmem + 128, kmaj(va, BN, kk), kmaj(da, BM, kk), idS, kk > 0);
+                umma_commit(BAR(SS_FULL));
+            }
+            grad_mma(ns - 1);
+            umma_commit(BAR(OUT_FULL));
+        }
+        __syncwarp();
+    } else if (warp == 9) {
+        // ==================== TMA: V tile once, dO tiles per step ====================
+        if (lane == 0 && ns > 0) {
+            mbar_arrive_expect_tx(BAR(KV_FULL), BN * DV * 2);
+#pragma unroll
+            for (int cb = 0; cb < DV / 64; ++cb)
+                tma_load_3d(sb + C::OFF_V + cb * BN * 128, &tm_v, BAR(KV_FULL), cb * 64, jb * BN, b * a.H_kv + g);
+            for (int s = 0; s < ns; ++s) {
+                const int st = s & 1, u = s >> 1;
+                const int h = g * R + s / nib, ib = ib0 + s % nib;
+                mbar_wait(BAR(DOO_EMPTY + st), (u & 1) ^ 1);
+                mbar_arrive_expect_tx(BAR(DOO_FULL + st), BM * DV * 2);
+#pragma unroll
+                for (int cb = 0; cb < DV / 64; ++cb)
+                    tma_load_3d(sb + C::OFF_DO + st * BM * DV * 2 + cb * BM * 128, &tm_do, BAR(DOO_FULL + st), cb * 64,
+                                ib * BM, b * a.H + h);
+            }
+        }
+        __syncwarp();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 8) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem);
+    }
+#undef BAR
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void *f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+// bf16 [planes][rows][dv] as 3-D TMA map, box 64 x 128 rows, 128B swizzle (zero fill past `rows`)
+bool make_map(CUtensorMap *tm, const void *base, int dv, int64_t rows, int64_t planes) {
+    auto encode = get_encode();
+    if (!encode) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)dv, (cuuint64_t)rows, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {(cuuint64_t)dv * 2, (cuuint64_t)rows * dv * 2};
+    cuuint32_t box[3] = {64, 128, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return encode(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int D, int DV>
+cudaError_t launch_bwd_t(const BwdArgs &a, const CUtensorMap &tv, const CUtensorMap &tdo, cudaStream_t st) {
+    using CQ = DqCfg<D, DV>;
+    using CK = KvCfg<D, DV>;
+    auto kq = bwd_dq_kernel<D, DV>;
+    auto kk = bwd_dkdv_kernel<D, DV>;
+    cudaError_t e = cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, CQ::SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize, CK::SMEM);
+    if (e != cudaSuccess) return e;
+    const int64_t nq_items = (int64_t)a.B * a.H * a.nqb, nk_items = (int64_t)a.B * a.H_kv * a.nkt;
+    if (nq_items > INT32_MAX || nk_items > INT32_MAX) return cudaErrorNotSupported;
+    if (nk_items > 0) kk<<<(unsigned)nk_items, NTH, CK::SMEM, st>>>(tv, tdo, a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (nq_items > 0) kq<<<(unsigned)nq_items, NTH, CQ::SMEM, st>>>(tv, tdo, a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_attn_bwd(const AttnParams &p, int d, int d_v, const void *dO, float *Dws, float *dq, float *dk,
+                            float *dv, cudaStream_t st) {
+    if ((d != 64 && d != 128) || (d_v != 64 && d_v != 128)) return cudaErrorNotSupported;
+    const int64_t rows = (int64_t)p.B * p.H * p.n_q;
+    if (rows > 0) {
+        bwd_prep_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(static_cast<const uint16_t *>(p.o),
+                                                                   static_cast<const uint16_t *>(dO), rows, d_v, Dws);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    BwdArgs a;
+    a.q_idx = p.q_idx;
+    a.k_idx = p.k_idx;
+    a.q_val = static_cast<const uint16_t *>(p.q_val);
+    a.k_val = static_cast<const uint16_t *>(p.k_val);
+    a.lse = p.lse;
+    a.Dr = Dws;
+    a.dq = dq;
+    a.dk = dk;
+    a.dv = dv;
+    a.B = p.B;
+    a.H = p.H;
+    a.H_kv = p.H_kv;
+    a.k = p.k;
+    a.n_q = p.n_q;
+    a.n_kv = p.n_kv;
+    a.q_pos0 = p.q_pos0;
+    a.causal = p.causal;
+    a.nqb = (int)((p.n_q + BM - 1) / BM);
+    a.nkt = (int)((p.n_kv + BN - 1) / BN);
+    a.c_scale = p.scale_log2;
+    a.scale = p.scale_log2 / 1.4426950408889634f;
+    CUtensorMap tv, tdo;
+    if (!make_map(&tv, p.v, d_v, p.n_kv, (int64_t)p.B * p.H_kv) || !make_map(&tdo, dO, d_v, p.n_q, (int64_t)p.B * p.H))
+        return cudaErrorInvalidValue;
+    if (d == 64) return d_v == 64 ? launch_bwd_t<64, 64>(a, tv, tdo, st) : launch_bwd_t<64, 128>(a, tv, tdo, st);
+    return d_v == 64 ? launch_bwd_t<128, 64>(a, tv, tdo, st) : launch_bwd_t<128, 128>(a, tv, tdo, st);
+}
+
+}  // namespace sfa

@@ -48,5 +48,9 @@ cudaError_t launch_attn_sm100_pair(const AttnParams &p, int d, int d_v, cudaStre
 // the same forward with 256-key score tiles and P apart from S (attn_sm100_wide.cu)
 cudaError_t launch_attn_sm100_wide(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
 cudaError_t launch_attn_sm100_ot(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
+// backward with the straight-through rule (bwd.cu): D = rowsum(dO . O) into Dws [B*H*n_q], then the
+// dK~/dV and dQ~ tensor-core kernels; gradients w.r.t. the code values and V, fp32
+cudaError_t launch_attn_bwd(const AttnParams &p, int d, int d_v, const void *dO, float *Dws, float *dq, float *dk,
+                            float *dv, cudaStream_t st);
 
 }  // namespace sfa

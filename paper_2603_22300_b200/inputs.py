@@ -21,7 +21,7 @@ from __future__ import annotations
 import numpy as np
 
 MASK64 = np.uint64(0xFFFFFFFFFFFFFFFF)
-TID_Q, TID_K, TID_V = 1, 2, 3
+TID_Q, TID_K, TID_V, TID_DO = 1, 2, 3, 4  # TID_DO: upstream gradient dO of the backward
 
 
 def splitmix64(x: np.ndarray) -> np.ndarray:

@@ -71,6 +71,8 @@ def lib() -> ctypes.CDLL:
             "sfa_device_supported": ([], I32),
             "sfa_debug_sm100_scores": ([D, P, P, P, P, P, P, P, P, SZ, P, P], I32),
             "sfa_gen_fill": ([P, I32, I64, I64, ctypes.c_uint64, I32, I32, I64, I32, I32, P], I32),
+            "sfa_attn_bwd_workspace_bytes": ([D], SZ),
+            "sfa_attn_bwd": ([D, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -83,7 +85,8 @@ EXPORTS = ("sfa_status_string", "sfa_topk_codes", "sfa_attn_workspace_bytes", "s
            "sfa_attn_fwd_bucketed", "sfa_key_tile", "sfa_forward_scratch_bytes", "sfa_forward",
            "sfa_forward_host", "sfa_device_supported", "sfa_gen_fill", "sfa_debug_sm100_scores",
            "sfa_attn_prepare", "sfa_attn_fwd_prepared", "sfa_dist_unique_id", "sfa_dist_init", "sfa_dist_destroy",
-           "sfa_dist_staging_bytes", "sfa_dist_allgather_kv", "sfa_dist_unpack_zigzag", "sfa_forward_host_pipelined")
+           "sfa_dist_staging_bytes", "sfa_dist_allgather_kv", "sfa_dist_unpack_zigzag", "sfa_forward_host_pipelined",
+           "sfa_attn_bwd_workspace_bytes", "sfa_attn_bwd")
 
 
 def _check(code: int, where: str):
@@ -208,6 +211,28 @@ def debug_sm100_scores(q_idx, q_val, k_idx, k_val, v, *, d, causal=True, scale=N
                                         _p(o), _p(lse), _p(ws), ws.numel(), _p(S), _stream()),
            "sfa_debug_sm100_scores")
     return o, lse, S[:128 * 128].view(128, 128), S[128 * 128:]
+
+
+def attn_bwd(q_idx, q_val, k_idx, k_val, v, o, lse, dO, *, d, causal=True, scale=None, q_pos0=0, workspace=None,
+             out=None):
+    """Backward with the straight-through rule (include/sfa.h sfa_attn_bwd): returns fp32
+    (dq_val [B,H,n_q,k], dk_val [B,H_kv,n_kv,k], dv [B,H_kv,n_kv,d_v])."""
+    _dev(q_idx, q_val, k_idx, k_val, v, o, lse, dO)
+    desc = _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, KERNEL_AUTO, _dt(v))
+    B, H, n_q, k = q_idx.shape
+    _, H_kv, n_kv, _ = k_idx.shape
+    if workspace is None:
+        workspace = torch.empty(max(int(lib().sfa_attn_bwd_workspace_bytes(ctypes.byref(desc))), 16),
+                                dtype=torch.uint8, device=v.device)
+    if out is None:
+        f32 = dict(dtype=torch.float32, device=v.device)
+        out = (torch.empty((B, H, n_q, k), **f32), torch.empty((B, H_kv, n_kv, k), **f32),
+               torch.empty((B, H_kv, n_kv, v.shape[-1]), **f32))
+    dq, dk, dv = out
+    _check(lib().sfa_attn_bwd(ctypes.byref(desc), _p(q_idx), _p(q_val), _p(k_idx), _p(k_val), _p(v), _p(o), _p(lse),
+                              _p(dO), _p(dq), _p(dk), _p(dv), _p(workspace), workspace.numel(), _stream()),
+           "sfa_attn_bwd")
+    return dq, dk, dv
 
 
 def scratch_bytes(desc: AttnDesc) -> int:

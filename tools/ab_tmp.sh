@@ -1,8 +1,5 @@
 mkdir -p gpurun_out
 python -m paper_2603_22300_b200.build --force >/dev/null
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$? $(tail -1 gpurun_out/pytest_gpu.log)"
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
-timeout 300 python bench.py > gpurun_out/bench_default.json 2>gpurun_out/bench_default.err; echo "bench rc=$?"
-grep -o '"attn": [0-9.]*' gpurun_out/bench_default.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_ot.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_sm100_ot -s 1 -c 1 -o gpurun_out/ot_final -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+timeout 600 python -m pytest tests/test_gpu_bwd.py -m gpu -x -q > gpurun_out/t_bwd.log 2>&1; echo "pytest rc=$? $(tail -1 gpurun_out/t_bwd.log)"
+timeout 600 python bench.py --mode bwd --steps 5 --warmup 3 > gpurun_out/bench_bwd.json 2>gpurun_out/bench_bwd.err; echo "bench rc=$?"; cat gpurun_out/bench_bwd.json | head -c 1500; tail -3 gpurun_out/bench_bwd.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bwd.csv python bench.py --mode bwd --steps 1 --warmup 1 > /dev/null 2>&1; echo "ncu rc=$?"
