@@ -112,13 +112,14 @@ __global__ void __launch_bounds__(256) topk_codes_kernel(const Bits *__restrict_
 // row and is ALU-bound at ~9% of HBM bandwidth).  A CTA of 128 threads owns 128 consecutive rows:
 //   1. coalesced 16-byte loads of the rows into shared memory, 16-byte chunks XOR-swizzled by
 //      (row & 15) so each thread then reads its own row with conflict-free LDS.128;
-//   2. the row as 64 (d=128) or 32 (d=64) registers of two bf16 each; kh = bits | 0x80008000
-//      holds both 15-bit magnitude keys with a guard bit, so (kh - T*0x10001) has bit 15 / 31 set
-//      exactly when key >= T (no borrow crosses the halves);
-//   3. the same bitwise binary search for the k-th largest key T (15 steps), counting with
-//      one subtract + mask + popc per 4 keys;
-//   4. keys > T, then ties == T lowest index first (A2), in ascending feature order (A4), staged
-//      in shared memory and written out with coalesced stores.
+//   2. the row as 64 (d=128) or 32 (d=64) registers of two |bf16| bit patterns each (sign cleared:
+//      for finite non-negative bf16 the numeric order IS the order of the 15-bit keys);
+//   3. the same bitwise binary search for the k-th largest key T (15 steps), counting on the FP16
+//      pipe: set.ge.bf16x2 (1.0 per key >= T) + add.bf16x2 into four exact accumulators, 2
+//      instructions per 2 keys (the integer subtract/popc version kept the ALU pipe at 82 %);
+//   4. selection bit masks (set.ge against T + 1, set.eq against T), ties == T taken lowest index
+//      first (A2), then the set bits walked in ascending feature order (A4) with the values
+//      re-read from the row in shared memory; staged and written out with coalesced stores.
 // Non-finite inputs: max key (max.u16x2) >= 0x7F80.
 constexpr int TK_ROWS = 128;
 
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(TK_ROWS) topk_rows_bf16_kernel(const uint16_t 
     __syncthreads();
 
     const bool active = t < nrows;
-    uint32_t kh[NW];
+    uint32_t ab[NW];  // |x| bit patterns, two keys per word
     uint32_t mx2 = 0;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -154,25 +155,32 @@ __global__ void __launch_bounds__(TK_ROWS) topk_rows_bf16_kernel(const uint16_t 
         const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            kh[4 * c + e] = ww[e] | 0x80008000u;
+            ab[4 * c + e] = ww[e] & 0x7FFF7FFFu;
             uint32_t m;
-            asm("max.u16x2 %0, %1, %2;" : "=r"(m) : "r"(mx2), "r"(ww[e] & 0x7FFF7FFFu));
+            asm("max.u16x2 %0, %1, %2;" : "=r"(m) : "r"(mx2), "r"(ab[4 * c + e]));
             mx2 = m;
         }
     }
     const uint32_t mx = max(mx2 & 0xFFFFu, mx2 >> 16);
     if (active && mx >= 0x7F80u && status_word != nullptr) atomicOr(status_word, 1u);
 
-    // #{key >= T} over the row
+    // #{key >= T} over the row, on the FP16 pipe: for finite non-negative bf16 the numeric order is the
+    // order of the bit patterns (subnormals kept: no .ftz), so set.ge.bf16x2 gives 1.0 per key >= T and
+    // four bf16x2 accumulators count exactly (<= 32 per half).  Non-finite rows are flagged above.
     auto count_ge = [&](uint32_t T) {
         const uint32_t t2 = T * 0x10001u;
-        int cnt = 0;
+        uint32_t acc[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int i = 0; i < NW; i += 2) {
-            const uint32_t a = (kh[i] - t2) & 0x80008000u, b = (kh[i + 1] - t2) & 0x80008000u;
-            cnt += __popc((a >> 1) | b);
+        for (int i = 0; i < NW; ++i) {
+            uint32_t m;
+            asm("set.ge.bf16x2.bf16x2 %0, %1, %2;" : "=r"(m) : "r"(ab[i]), "r"(t2));
+            asm("add.rn.bf16x2 %0, %0, %1;" : "+r"(acc[i & 3]) : "r"(m));
         }
-        return cnt;
+        uint32_t s01, s23, s;
+        asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(s01) : "r"(acc[0]), "r"(acc[1]));
+        asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(s23) : "r"(acc[2]), "r"(acc[3]));
+        asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(s) : "r"(s01), "r"(s23));  // <= 64 per half: exact
+        return (int)(__uint_as_float(s << 16) + __uint_as_float(s & 0xFFFF0000u));
     };
     // 3. largest T with #{key >= T} >= k
     uint32_t T = 0;
@@ -181,27 +189,44 @@ __global__ void __launch_bounds__(TK_ROWS) topk_rows_bf16_kernel(const uint16_t 
         const uint32_t cand = T | (1u << bit);
         if (count_ge(cand) >= k) T = cand;
     }
-    int ties = k - count_ge(T + 1);  // >= 1 ties at T to take, lowest index first
-    // 4. ascending compaction into the staging area
+    // 4. selection bit masks (bit f = key f): key > T always, key == T for the lowest-index ties
+    constexpr int NM = D / 32;
+    uint32_t gm[NM], em[NM];
+#pragma unroll
+    for (int w = 0; w < NM; ++w) gm[w] = em[w] = 0u;
+    const uint32_t tg = (T + 1u) * 0x10001u, te = T * 0x10001u;  // T + 1 <= 0x7F80 (+inf) on finite rows
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+        uint32_t g, e;  // bf16 1.0 (0x3F80, bit 7 set) per true half
+        asm("set.ge.bf16x2.bf16x2 %0, %1, %2;" : "=r"(g) : "r"(ab[i]), "r"(tg));
+        asm("set.eq.bf16x2.bf16x2 %0, %1, %2;" : "=r"(e) : "r"(ab[i]), "r"(te));
+        gm[i >> 4] |= (((g >> 7) & 1u) | ((g >> 22) & 2u)) << (2 * (i & 15));
+        em[i >> 4] |= (((e >> 7) & 1u) | ((e >> 22) & 2u)) << (2 * (i & 15));
+    }
+    int need = k;
+#pragma unroll
+    for (int w = 0; w < NM; ++w) need -= __popc(gm[w]);
+#pragma unroll
+    for (int w = 0; w < NM; ++w)
+        while (need > 0 && em[w] != 0u) {  // lowest-index ties first (A2)
+            gm[w] |= em[w] & (0u - em[w]);
+            em[w] &= em[w] - 1u;
+            --need;
+        }
+    // 5. ascending compaction into the staging area (values re-read from the row in shared memory)
     uint8_t *my_i = oidx + t * k;
     uint16_t *my_v = oval + t * k;
     int pos = 0;
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        const uint4 w = *reinterpret_cast<const uint4 *>(rowbuf + t * D * 2 + ((c ^ (t & 15) & (NC - 1)) << 4));
-        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const uint32_t bits = (ww[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
-            const uint32_t key = bits & 0x7FFFu;
-            const bool tie = key == T;
-            const bool sel = key > T || (tie && ties > 0);
-            ties -= (tie && sel) ? 1 : 0;
-            if (sel && active) {
-                my_i[pos] = (uint8_t)(8 * c + e);
-                my_v[pos] = (uint16_t)bits;
-            }
-            pos += sel ? 1 : 0;
+    for (int w = 0; w < NM; ++w) {
+        uint32_t m = active ? gm[w] : 0u;
+        while (m != 0u) {
+            const int f = 32 * w + (__ffs(m) - 1);
+            m &= m - 1u;
+            const int c = f >> 3;
+            my_i[pos] = (uint8_t)f;
+            my_v[pos] = *reinterpret_cast<const uint16_t *>(rowbuf + t * D * 2 + ((c ^ (t & 15) & (NC - 1)) << 4) + (f & 7) * 2);
+            ++pos;
         }
     }
     __syncthreads();
