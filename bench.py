@@ -655,7 +655,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        r = oracle_sample(W, seed, 1024, 2048, threads)
+        # bounded sample of ~15 s of CPU work: a 1024-row probe sizes the timed sample
+        probe = oracle_sample(W, seed + 1, 1024, 2048, threads)
+        n_rows = int(max(1024, min(W.H * W.n // 2, 1024 * 16.0 / max(probe["t_sample"], 1e-3))))
+        r = oracle_sample(W, seed, n_rows, 2048, threads)
         cpu = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": threads, "kind": "oracle",
                "sample": r["sample"], "sample_seconds": r["t_sample"]}
     if rank == 0:

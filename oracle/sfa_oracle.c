@@ -30,6 +30,14 @@
  *                    two passes over the materialised row, fp64 throughout.
  *                    Rows with no allowed key: O_i = 0, LSE_i = -inf (A10).
  *
+ *                    edges_only = 1 (reading A1/R2; "Traversing active
+ *                    coordinates yields only the nonzero attention edges", P:L122 O(E + E d_v)):
+ *                    a pair (i, j) is kept only if it is allowed AND the supports intersect,
+ *                      edge(i,j) = exists t, t' : q_idx[i][t] == k_idx[j][t']
+ *                    (index equality; zero-valued selected entries count as support, A8); the
+ *                    softmax runs over the edges only; a row with no edge gets O = 0, LSE = -inf
+ *                    (as A10).
+ *
  *   ref_scores_row   the s_ij of one row (for the "rows of P sum to 1" pin).
  *
  *   ref_attn_bwd     the backward pass of ref_attn_fwd with the straight-through rule
@@ -139,7 +147,7 @@ int ref_topk_codes(const void *x, int dtype, int64_t rows, int d, int k, uint8_t
 
 /* ---- attention on the decompressed codes: P:L97-101, P:L43-50 ---------------------- */
 typedef struct {
-    int B, H, H_kv, d, k, d_v, causal, dtype;
+    int B, H, H_kv, d, k, d_v, causal, dtype, edges_only;
     int64_t n_q, n_kv, q_pos0;
     double scale;
     const uint8_t *q_idx, *k_idx;
@@ -155,6 +163,14 @@ typedef struct {
 static void densify(const uint8_t *idx, const void *val, int dtype, int64_t row, int k, int d, double *out) {
     for (int u = 0; u < d; ++u) out[u] = 0.0;
     for (int t = 0; t < k; ++t) out[idx[row * k + t]] = widen(val, dtype, row * k + t);
+}
+
+/* R2 (edges_only): do the supports of query row qrow and key row krow share a feature index? */
+static int supports_intersect(const uint8_t *q_idx, int64_t qrow, const uint8_t *k_idx, int64_t krow, int k) {
+    for (int t = 0; t < k; ++t)
+        for (int u = 0; u < k; ++u)
+            if (q_idx[qrow * k + t] == k_idx[krow * k + u]) return 1;
+    return 0;
 }
 
 static void attn_one_row(attn_job *J, int64_t flat, double *o, double *lse, double *qd, double *kd, double *s) {
@@ -173,14 +189,23 @@ static void attn_one_row(attn_job *J, int64_t flat, double *o, double *lse, doub
     densify(J->q_idx, J->q_val, J->dtype, flat, J->k, J->d, qd);
     double m = -INFINITY;
     for (int64_t j = 0; j <= jmax; ++j) {
+        if (J->edges_only && !supports_intersect(J->q_idx, flat, J->k_idx, kvrow0 + j, J->k)) {
+            s[j] = -INFINITY; /* R2: not an edge -> excluded from the softmax */
+            continue;
+        }
         densify(J->k_idx, J->k_val, J->dtype, kvrow0 + j, J->k, J->d, kd);
         double acc = 0.0;
         for (int u = 0; u < J->d; ++u) acc += qd[u] * kd[u];
         s[j] = J->scale * acc; /* A5/A17: scale applied after the sum */
         if (s[j] > m) m = s[j];
     }
+    if (m == -INFINITY) { /* R2 only: no edge in the row (as A10) */
+        *lse = -INFINITY;
+        return;
+    }
     double l = 0.0;
     for (int64_t j = 0; j <= jmax; ++j) {
+        if (s[j] == -INFINITY) continue;
         double p = exp(s[j] - m);
         l += p;
         for (int c = 0; c < J->d_v; ++c) o[c] += p * widen(J->v, J->dtype, (kvrow0 + j) * J->d_v + c);
@@ -217,10 +242,10 @@ static void *attn_worker(void *arg) {
     return NULL;
 }
 
-int ref_attn_fwd(int B, int H, int H_kv, int d, int k, int d_v, int64_t n_q, int64_t n_kv, int64_t q_pos0,
-                 int causal, double scale, int dtype, const uint8_t *q_idx, const void *q_val,
-                 const uint8_t *k_idx, const void *k_val, const void *v, const int64_t *sel, int64_t nsel,
-                 double *o, double *lse, int threads) {
+int ref_attn_fwd_ex(int B, int H, int H_kv, int d, int k, int d_v, int64_t n_q, int64_t n_kv, int64_t q_pos0,
+                    int causal, double scale, int dtype, const uint8_t *q_idx, const void *q_val,
+                    const uint8_t *k_idx, const void *k_val, const void *v, const int64_t *sel, int64_t nsel,
+                    double *o, double *lse, int threads, int edges_only) {
     if (B < 1 || H < 1 || H_kv < 1 || H % H_kv || d < 1 || d > 256 || k < 1 || k > d || d_v < 1 || n_q < 0 ||
         n_kv < 0 || dtype < 0 || dtype > 2 || !(scale > 0) || !isfinite(scale))
         return ORACLE_INVALID_ARGUMENT;
@@ -228,6 +253,7 @@ int ref_attn_fwd(int B, int H, int H_kv, int d, int k, int d_v, int64_t n_q, int
     memset(&J, 0, sizeof J);
     J.B = B; J.H = H; J.H_kv = H_kv; J.d = d; J.k = k; J.d_v = d_v; J.causal = causal; J.dtype = dtype;
     J.n_q = n_q; J.n_kv = n_kv; J.q_pos0 = q_pos0; J.scale = scale;
+    J.edges_only = edges_only != 0;
     J.q_idx = q_idx; J.k_idx = k_idx; J.q_val = q_val; J.k_val = k_val; J.v = v;
     J.sel = sel;
     J.nsel = sel ? nsel : (int64_t)B * H * n_q;
@@ -240,6 +266,14 @@ int ref_attn_fwd(int B, int H, int H_kv, int d, int k, int d_v, int64_t n_q, int
     for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
     pthread_mutex_destroy(&J.mu);
     return J.status;
+}
+
+int ref_attn_fwd(int B, int H, int H_kv, int d, int k, int d_v, int64_t n_q, int64_t n_kv, int64_t q_pos0,
+                 int causal, double scale, int dtype, const uint8_t *q_idx, const void *q_val,
+                 const uint8_t *k_idx, const void *k_val, const void *v, const int64_t *sel, int64_t nsel,
+                 double *o, double *lse, int threads) {
+    return ref_attn_fwd_ex(B, H, H_kv, d, k, d_v, n_q, n_kv, q_pos0, causal, scale, dtype, q_idx, q_val, k_idx,
+                           k_val, v, sel, nsel, o, lse, threads, 0);
 }
 
 /* s_ij for j = 0..n_kv-1 of one query row (flat id into [B][H][n_q]); masked keys get -inf. */
