@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--config", default="qwen3", choices=sorted(accounting.CONFIGS))
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "sm100", "pair", "wide", "ot"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--edges-only", action="store_true",
+                    help="reading A1/R2 (SURVEY 8(f) N4): only pairs whose supports intersect enter the softmax")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--k", type=int, default=None, help="override the code size k (sweep)")
     ap.add_argument("--mode", default="forward", choices=["forward", "decode", "bwd"],
@@ -184,6 +186,7 @@ def config_of(args, W):
             "global_batch": W.B * args.gpus, "seq_len": W.n, "parallelism": f"weak: batch element r on rank r "
             f"({args.gpus} GPU{'s' if args.gpus > 1 else ''}), no data-path collective",
             "kernel": args.kernel,
+            "semantics": "R2 edges-only (A1/R2)" if getattr(args, "edges_only", False) else "R1 (A1)",
             "l2": f"explicit {L2_FLUSH_MB} MB write between timed steps (outside the step events); "
                   "inputs+outputs also exceed the 126 MB L2"}
 
@@ -520,7 +523,8 @@ def main():
     sfa.gen_fill(K, seed, inputs.TID_K, offset=rank * K.numel())
     sfa.gen_fill(V, seed, inputs.TID_V, offset=rank * V.numel())
     desc = sfa.make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k, d_v=d_v, n_q=n, n_kv=n, causal=W.causal,
-                         dtype=sfa.SFA_BF16 if W.dtype == "bf16" else sfa.SFA_F32, kernel=kernel)
+                         dtype=sfa.SFA_BF16 if W.dtype == "bf16" else sfa.SFA_F32, kernel=kernel,
+                         edges_only=args.edges_only)
     q_idx = torch.empty((B, H, n, k), dtype=torch.uint8, device=dev)
     q_val = torch.empty((B, H, n, k), dtype=dt, device=dev)
     k_idx = torch.empty((B, H_kv, n, k), dtype=torch.uint8, device=dev)
@@ -672,7 +676,7 @@ def main():
                 "interactions_per_s": W.expected_interactions / (ms_per_step / 1e3) * world,
                 "pairs_per_s": pairs * world / (ms_per_step / 1e3),
                 "wall_s_timed_region": t_wall,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (5 if sm100 else 4) * args.steps,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (5 + int(args.edges_only) if sm100 else 4) * args.steps,
                 "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -98,13 +98,21 @@ typedef struct {
     float scale;         /* logit multiplier; > 0 and finite; the paper's is 1/sqrt(d) (A5)         */
     sfa_dtype dtype;     /* dtype of q_val, k_val, v and o (LSE is always fp32)                            */
     int32_t kernel;      /* sfa_kernel; SFA_KERNEL_AUTO unless benchmarking an ablation                   */
+    int32_t edges_only;  /* 0: reading A1/R1 (default) -- every allowed pair enters the softmax, a pair with
+                            disjoint supports with logit 0 ("mathematically identical
+                            to softmax(Q~K~^T/sqrt d)V").  1: R2 -- only the "nonzero
+                            attention edges": pair (i, j) enters iff the supports share
+                            a feature index (zero-valued selected entries count, A8); a row with no edge
+                            gets O = 0, LSE = -inf.  R2 runs on SM100_OT (bf16, d_v = 128) and SIMT
+                            (AUTO picks them); other explicit kernels -> SFA_ERR_UNSUPPORTED.          */
 } sfa_attn_desc;
 
 /* Bytes of device workspace sfa_attn_fwd needs (0 on an invalid desc):
  *   SIMT kernel : the key-tile feature buckets (our form of the
  *                 paper's CSC_feat);
  *   SM100 kernel: max|V| per (b, kv head) + an fp16 copy of V scaled by a power of two per
- *                 (b, kv head) -- the exact fp16 P.V operand (reading A12);
+ *                 (b, kv head) -- the exact fp16 P.V operand (reading A12); with
+ *                 edges_only also, per 128-key tile, a 128-bit key set per feature (edges.cu);
  *   DECODE kernel: one fp32 partial (max, sum, O) per (b, kv head, key split) for the merge. */
 SFA_API size_t sfa_attn_workspace_bytes(const sfa_attn_desc *desc);
 

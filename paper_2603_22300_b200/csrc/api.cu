@@ -38,6 +38,10 @@ sfa_status validate_desc(const sfa_attn_desc *d) {
         (d->dtype != SFA_BF16 || (int64_t)(d->H / d->H_kv) * d->n_q > 16))
         return SFA_ERR_UNSUPPORTED;
     if ((d->n_kv + 63) / 64 > (int64_t)INT32_MAX) return SFA_ERR_UNSUPPORTED;
+    if (d->edges_only != 0 && d->edges_only != 1) return SFA_ERR_INVALID_ARGUMENT;
+    if (d->edges_only && d->kernel != SFA_KERNEL_AUTO && d->kernel != SFA_KERNEL_SIMT &&
+        d->kernel != SFA_KERNEL_SM100_OT)
+        return SFA_ERR_UNSUPPORTED;  // R2 is built into the OT and SIMT kernels only
     return SFA_OK;
 }
 
@@ -51,6 +55,7 @@ BucketLayout layout_of(const sfa_attn_desc *d) {
 int resolve_kernel(const sfa_attn_desc *d) {
     if (d->kernel == SFA_KERNEL_SIMT || d->dtype == SFA_F32) return SFA_KERNEL_SIMT;
     if (d->kernel != SFA_KERNEL_AUTO) return d->kernel;
+    if (d->edges_only) return d->d_v == 128 ? SFA_KERNEL_SM100_OT : SFA_KERNEL_SIMT;  // R2 kernels
     if ((int64_t)(d->H / d->H_kv) * d->n_q <= 16) return SFA_KERNEL_DECODE;
     return d->d_v == 128 ? SFA_KERNEL_SM100_OT : SFA_KERNEL_SM100;
 }
@@ -67,10 +72,13 @@ size_t vprep_amax_bytes(const sfa_attn_desc *d) { return align_up((int64_t)d->B 
 size_t vprep_bytes(const sfa_attn_desc *d) {
     return vprep_amax_bytes(d) + (size_t)d->B * d->H_kv * d->n_kv * d->d_v * 2;
 }
+// R2 on SM100_OT: the key-tile feature bitsets (edges.cu) follow the V prep, 256-aligned
+bool uses_kmask(const sfa_attn_desc *d) { return d->edges_only && resolve_kernel(d) == SFA_KERNEL_SM100_OT; }
 size_t ws_bytes(const sfa_attn_desc *d) {
     const int kern = resolve_kernel(d);
     if (kern == SFA_KERNEL_SIMT) return bucket_bytes(d);
     if (kern == SFA_KERNEL_DECODE) return decode_workspace_bytes((int64_t)d->B * d->H_kv, d->n_kv, d->d_v);
+    if (uses_kmask(d)) return align_up(vprep_bytes(d), 256) + kfmask_bytes((int64_t)d->B * d->H_kv, d->n_kv, d->d);
     return vprep_bytes(d);
 }
 
@@ -105,6 +113,8 @@ AttnParams make_params(const sfa_attn_desc *d, const uint8_t *q_idx, const void 
     p.n_q = d->n_q; p.n_kv = d->n_kv; p.q_pos0 = d->q_pos0; p.causal = d->causal;
     p.scale_log2 = d->scale * kLog2e;
     p.L = layout_of(d);
+    p.edges_only = d->edges_only;
+    p.kfmask = (ws && uses_kmask(d)) ? (const uint32_t *)((const uint8_t *)ws + align_up(vprep_bytes(d), 256)) : nullptr;
     return p;
 }
 
@@ -123,7 +133,10 @@ sfa_status run_prepare(const sfa_attn_desc *d, const uint8_t *k_idx, const void 
     if (uses_simt(d))
         return from_cuda(launch_bucket(k_idx, k_val, d->dtype == SFA_BF16, d->d, d->k, (int64_t)d->B * d->H_kv,
                                        d->n_kv, p.L, ws, st));
-    return from_cuda(launch_vprep(v, (int64_t)d->B * d->H_kv, d->n_kv, d->d_v, (uint32_t *)p.v_amax, (void *)p.v16, st));
+    cudaError_t e = launch_vprep(v, (int64_t)d->B * d->H_kv, d->n_kv, d->d_v, (uint32_t *)p.v_amax, (void *)p.v16, st);
+    if (e == cudaSuccess && uses_kmask(d))
+        e = launch_kfmask(k_idx, (int64_t)d->B * d->H_kv, d->n_kv, d->d, d->k, (uint32_t *)p.kfmask, st);
+    return from_cuda(e);
 }
 
 // steps 4-8 over a prepared workspace

@@ -14,11 +14,18 @@
 //           re-zeroed in the same pass.
 //   step 7  O += p * V_j with V_j broadcast from shared memory (fp32 accumulate in registers).
 //   step 8  O /= l, round to the output dtype (RNE); LSE = (m + log2 l) ln 2.
+// EDGE (reading A1/R2): the scatter itself finds the edges -- P:L101 "Traversing
+// active coordinates yields only the nonzero attention edges".  Slab entries start as the
+// sentinel UNTOUCHED (a NaN bit pattern no fmaf produces from finite inputs); the first product
+// that lands on (j, lane) replaces it, so after the scatter an entry still UNTOUCHED is a pair with
+// disjoint supports and is left out of the softmax (zero-valued support entries still touch: A8).
 #include "launch.cuh"
 
 namespace sfa {
 
-template <typename T, int D, int DV, int BK>
+constexpr uint32_t UNTOUCHED = 0xFFFFFFFFu;
+
+template <typename T, int D, int DV, int BK, bool EDGE>
 __global__ void __launch_bounds__(128) attn_simt_kernel(const AttnParams p) {
     constexpr bool kBF16 = DT<T>::is_bf16;
     constexpr int EB = kBF16 ? 4 : 8;
@@ -41,7 +48,8 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const AttnParams p) {
     float *slab = slab_all + w * (BK + 1) * 32 + lane;
     const uint16_t *off = reinterpret_cast<const uint16_t *>(btile);
 
-    for (int i = tid; i < 4 * (BK + 1) * 32; i += 128) slab_all[i] = 0.f;
+    const float slab_init = EDGE ? __uint_as_float(UNTOUCHED) : 0.f;
+    for (int i = tid; i < 4 * (BK + 1) * 32; i += 128) slab_all[i] = slab_init;
 
     const int64_t last_row = ((int64_t)qb * 128 + 127 < p.n_q - 1) ? (int64_t)qb * 128 + 127 : p.n_q - 1;
     int ntiles = p.L.ntiles;
@@ -87,14 +95,16 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const AttnParams p) {
                     for (int e = e0; e < e1; ++e) {
                         const uint32_t x = ent[e];
                         float *s = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(slab) + (x & 0xFFFFu));
-                        *s = fmaf(q, __uint_as_float(x & 0xFFFF0000u), *s);
+                        const float cur = *s;
+                        *s = fmaf(q, __uint_as_float(x & 0xFFFF0000u), (EDGE && __float_as_uint(cur) == UNTOUCHED) ? 0.f : cur);
                     }
                 } else {
                     const uint2 *ent = reinterpret_cast<const uint2 *>(btile + p.L.off_bytes);
                     for (int e = e0; e < e1; ++e) {
                         const uint2 x = ent[e];
                         float *s = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(slab) + x.x);
-                        *s = fmaf(q, __uint_as_float(x.y), *s);
+                        const float cur = *s;
+                        *s = fmaf(q, __uint_as_float(x.y), (EDGE && __float_as_uint(cur) == UNTOUCHED) ? 0.f : cur);
                     }
                 }
             }
@@ -105,7 +115,10 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const AttnParams p) {
             if (jv > BK) jv = BK;
             // step 6: online softmax (log2 domain)
             float mx = -INFINITY;
-            for (int j = 0; j < jv; ++j) mx = fmaxf(mx, slab[j * 32]);
+            for (int j = 0; j < jv; ++j) {
+                const float sj = slab[j * 32];
+                if (!EDGE || __float_as_uint(sj) != UNTOUCHED) mx = fmaxf(mx, sj);
+            }
             if (mx > m) {
                 const float alpha = fast_exp2(m - mx);  // m = -inf -> 0
                 l *= alpha;
@@ -116,8 +129,8 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const AttnParams p) {
             // steps 6-7: p = 2^(s - m), l += p, O += p V_j ; re-zero the slab
             for (int j = 0; j < BK; ++j) {
                 const float s = slab[j * 32];
-                slab[j * 32] = 0.f;
-                if (j < jv) {
+                slab[j * 32] = slab_init;
+                if (j < jv && (!EDGE || __float_as_uint(s) != UNTOUCHED)) {
                     const float pj = fast_exp2(s - m);
                     l += pj;
                     const T *vr = Vs + j * DV;
@@ -174,7 +187,7 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const AttnParams p) {
 template <typename T, int D, int DV, int BK>
 static cudaError_t launch_simt_t(const AttnParams &p, cudaStream_t stream) {
     const size_t smem = 4 * (BK + 1) * 32 * 4 + p.L.tile_bytes + (size_t)BK * DV * sizeof(T);
-    auto kern = attn_simt_kernel<T, D, DV, BK>;
+    auto kern = p.edges_only ? attn_simt_kernel<T, D, DV, BK, true> : attn_simt_kernel<T, D, DV, BK, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((p.n_q + 127) / 128), (unsigned)(p.B * p.H));

@@ -132,7 +132,15 @@ __device__ __forceinline__ void decode_item(const OtArgs &a, int item, int &b, T
 #define TLREC(tag) do {} while (0)
 #endif
 
-template <int D, bool DBG>
+__device__ __forceinline__ void prefetch_l1(const void *ptr) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr));
+}
+
+// EDGE (reading A1/R2, edges.cu): a pair enters the softmax only if the supports intersect.  Per key
+// tile each softmax thread ORs the tile's feature bitsets kf[f] over the k features of its row:
+// eh[q] bit c = "key 32q+c shares a feature with this row" (k 16-byte loads, issued before the
+// wait for S), ANDs in the causal / ragged bound, and excludes the other keys like the causal mask.
+template <int D, bool DBG, bool EDGE>
 __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid_constant__ CUtensorMap tmap_v,
                                                                       const OtArgs a) {
     using C = Cfg<D>;
@@ -193,14 +201,56 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         float *f_t = fac + t * BM;
         const uint32_t prow = sbase + C::OFF_P + (uint32_t)(t * BM + r) * 128u;  // row t*128+r, key atom 0
         const int bar_id = 1 + t;
+        const uint8_t *qi_row = p.q_idx + (((int64_t)b * p.H + tl[t].h) * p.n_q + (row_ok ? i : 0)) * p.k;
+        const uint4 *kf_head = reinterpret_cast<const uint4 *>(p.kfmask) + (int64_t)(b * p.H_kv + g) * a.nkt * D;
+        // EDGE, k <= 16: the row's feature indices stay in registers (4 x 4 bytes), so the k bitset
+        // loads of a tile are independent and issue back to back
+        uint32_t qw[4] = {0u, 0u, 0u, 0u};
+        if (EDGE && row_ok && p.k <= 16)
+            for (int u = 0; u < p.k; ++u) qw[u >> 2] |= (uint32_t)__ldg(qi_row + u) << (8 * (u & 3));
+        if (EDGE && lane < 2 * (D / 16)) prefetch_l1(kf_head + lane * 8);  // tile 0: D x 16 bytes of bitsets
         float m = -INFINITY, l = 0.f;
         for (int j = 0; j < nt; ++j) {
+            int64_t lim64 = kend - (int64_t)j * BN;
+            const int lim = lim64 < 0 ? 0 : (lim64 > BN ? BN : (int)lim64);
+            uint32_t eh[4];
+            if (EDGE) {
+                const uint4 *kf = kf_head + (int64_t)j * D;
+                uint4 h = make_uint4(0u, 0u, 0u, 0u);
+                if (row_ok && p.k <= 16) {
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        if (u < p.k) {
+                            const uint4 x = __ldg(kf + ((qw[u >> 2] >> (8 * (u & 3))) & 0xFFu));
+                            h.x |= x.x;
+                            h.y |= x.y;
+                            h.z |= x.z;
+                            h.w |= x.w;
+                        }
+                    }
+                } else if (row_ok) {
+#pragma unroll 4
+                    for (int u = 0; u < p.k; ++u) {
+                        const uint4 x = __ldg(kf + __ldg(qi_row + u));
+                        h.x |= x.x;
+                        h.y |= x.y;
+                        h.z |= x.z;
+                        h.w |= x.w;
+                    }
+                }
+                // the next tile's bitsets into L1 while this tile's softmax runs
+                if (j + 1 < nt && lane < 2 * (D / 16)) prefetch_l1(kf + D + lane * 8);
+                const uint32_t hw[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int rem = lim - 32 * q;  // step 5 folded in: keys at or past lim are excluded
+                    eh[q] = hw[q] & (rem >= 32 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : ((1u << rem) - 1u)));
+                }
+            }
             mbar_wait(BAR(SFULL + t), j & 1);
             if (lane == 0 && wq == 0) TLREC(0x1000 | (t << 10) | (j & 1023));
             tc_fence_after();
             uint32_t s[4][32];
-            int64_t lim64 = kend - (int64_t)j * BN;
-            const int lim = lim64 < 0 ? 0 : (lim64 > BN ? BN : (int)lim64);
             float mq[4];  // four independent max chains; keys 64-127 load while 0-63 are reduced
             tmem_ld32(tS, s[0]);
             tmem_ld32(tS + 32, s[1]);
@@ -209,6 +259,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
             tmem_ld32(tS + 96, s[3]);
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
+                if (EDGE) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c)
+                        if (!((eh[q] >> c) & 1u)) s[q][c] = 0xFF800000u;
+                }
                 mq[q] = -INFINITY;
 #pragma unroll
                 for (int c = 0; c < 32; ++c) mq[q] = fmaxf(mq[q], __uint_as_float(s[q][c]));
@@ -219,6 +274,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
             if (lane == 0) mbar_arrive(BAR(SEMPTY + t));  // S_t may be overwritten by S_t(j+1)
 #pragma unroll
             for (int q = 2; q < 4; ++q) {
+                if (EDGE) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c)
+                        if (!((eh[q] >> c) & 1u)) s[q][c] = 0xFF800000u;
+                }
                 mq[q] = -INFINITY;
 #pragma unroll
                 for (int c = 0; c < 32; ++c) mq[q] = fmaxf(mq[q], __uint_as_float(s[q][c]));
@@ -229,7 +289,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
 #pragma unroll
                     for (int c = 0; c < 32; ++c) a.dbg[r * BN + 32 * q + c] = __uint_as_float(s[q][c]);
             }
-            if (lim < BN) {  // step 5 on diagonal / ragged tiles: excluded keys -> -inf -> p = 0
+            if (!EDGE && lim < BN) {  // step 5 on diagonal / ragged tiles: excluded keys -> -inf -> p = 0
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     mq[q] = -INFINITY;
@@ -489,7 +549,8 @@ cudaError_t launch_t(const OtArgs &a, cudaStream_t stream, int items) {
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    auto kern = a.dbg != nullptr ? attn_sm100_ot_kernel<D, true> : attn_sm100_ot_kernel<D, false>;
+    auto kern = p.edges_only ? (a.dbg != nullptr ? attn_sm100_ot_kernel<D, true, true> : attn_sm100_ot_kernel<D, false, true>)
+                             : (a.dbg != nullptr ? attn_sm100_ot_kernel<D, true, false> : attn_sm100_ot_kernel<D, false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     kern<<<items, NTHREADS, C::SMEM, stream>>>(tm, a);
@@ -500,6 +561,7 @@ cudaError_t launch_t(const OtArgs &a, cudaStream_t stream, int items) {
 
 cudaError_t launch_attn_sm100_ot(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg) {
     if ((d != 64 && d != 128) || d_v != DV) return cudaErrorNotSupported;
+    if (p.edges_only && p.kfmask == nullptr) return cudaErrorInvalidValue;
     OtArgs a;
     a.p = p;
     a.nqb = (int)((p.n_q + BM - 1) / BM);

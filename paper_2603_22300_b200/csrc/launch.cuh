@@ -20,7 +20,14 @@ struct AttnParams {
     int32_t causal;
     float scale_log2;  // scale * log2(e): logits live in the log2 domain inside the kernels
     BucketLayout L;
+    int32_t edges_only;      // reading A1/R2: only pairs whose supports intersect enter the softmax
+    const uint32_t *kfmask;  // R2, SM100_OT: per key tile, per feature, the 128-bit set of keys selecting it
 };
+
+// R2 feature bitsets of the key tiles (edges.cu): [B*H_kv][ceil(n_kv/128)][d][4] u32
+size_t kfmask_bytes(int64_t bh_kv, int64_t n_kv, int d);
+cudaError_t launch_kfmask(const uint8_t *k_idx, int64_t bh_kv, int64_t n_kv, int d, int k, uint32_t *out,
+                          cudaStream_t stream);
 
 cudaError_t launch_topk(const void *x, bool bf16, int64_t rows, int d, int64_t ld, int k, uint8_t *idx, void *val,
                         uint32_t *status_word, cudaStream_t stream);

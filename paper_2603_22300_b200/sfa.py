@@ -34,7 +34,7 @@ class AttnDesc(ctypes.Structure):
                 ("d", ctypes.c_int32), ("k", ctypes.c_int32), ("d_v", ctypes.c_int32),
                 ("n_q", ctypes.c_int64), ("n_kv", ctypes.c_int64), ("q_pos0", ctypes.c_int64),
                 ("causal", ctypes.c_int32), ("scale", ctypes.c_float), ("dtype", ctypes.c_int32),
-                ("kernel", ctypes.c_int32)]
+                ("kernel", ctypes.c_int32), ("edges_only", ctypes.c_int32)]
 
 
 _lib = None
@@ -117,10 +117,12 @@ def _dev(*ts):
 
 
 def make_desc(*, B, H, H_kv, d, k, d_v, n_q, n_kv, q_pos0=0, causal=True, scale=None, dtype=SFA_BF16,
-              kernel=KERNEL_AUTO) -> AttnDesc:
+              kernel=KERNEL_AUTO, edges_only=False) -> AttnDesc:
+    """edges_only: reading A1/R2 (include/sfa.h) -- only pairs whose supports intersect."""
     if scale is None:
         scale = 1.0 / math.sqrt(d)  # P:L99, reading A5
-    return AttnDesc(B, H, H_kv, d, k, d_v, n_q, n_kv, q_pos0, int(bool(causal)), scale, dtype, kernel)
+    return AttnDesc(B, H, H_kv, d, k, d_v, n_q, n_kv, q_pos0, int(bool(causal)), scale, dtype, kernel,
+                    int(bool(edges_only)))
 
 
 def topk_codes(x: torch.Tensor, k: int, status: torch.Tensor | None = None):
@@ -135,11 +137,11 @@ def topk_codes(x: torch.Tensor, k: int, status: torch.Tensor | None = None):
     return idx, val
 
 
-def _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, kernel, dtype):
+def _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, kernel, dtype, edges_only=False):
     B, H, n_q, k = q_idx.shape
     _, H_kv, n_kv, _ = k_idx.shape
     return make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k, d_v=v.shape[-1], n_q=n_q, n_kv=n_kv, q_pos0=q_pos0,
-                     causal=causal, scale=scale, dtype=dtype, kernel=kernel)
+                     causal=causal, scale=scale, dtype=dtype, kernel=kernel, edges_only=edges_only)
 
 
 def workspace_bytes(desc: AttnDesc) -> int:
@@ -151,10 +153,11 @@ def key_tile(desc: AttnDesc) -> int:
 
 
 def attn_fwd(q_idx, q_val, k_idx, k_val, v, *, d, causal=True, scale=None, q_pos0=0, kernel=KERNEL_AUTO,
-             workspace=None, out=None):
-    """Stage 2: (O, LSE) = FlashSFA forward over the codes (bucketing + attention kernels)."""
+             workspace=None, out=None, edges_only=False):
+    """Stage 2: (O, LSE) = FlashSFA forward over the codes (bucketing + attention kernels).
+    edges_only: reading A1/R2 -- only the pairs whose supports intersect enter the softmax."""
     _dev(q_idx, q_val, k_idx, k_val, v)
-    desc = _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, kernel, _dt(v))
+    desc = _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, kernel, _dt(v), edges_only)
     B, H, n_q, _ = q_idx.shape
     nb = workspace_bytes(desc)
     if workspace is None:
@@ -239,13 +242,14 @@ def scratch_bytes(desc: AttnDesc) -> int:
     return int(lib().sfa_forward_scratch_bytes(ctypes.byref(desc)))
 
 
-def forward(q, k, v, *, k_code, causal=True, scale=None, q_pos0=0, kernel=KERNEL_AUTO, scratch=None, out=None):
+def forward(q, k, v, *, k_code, causal=True, scale=None, q_pos0=0, kernel=KERNEL_AUTO, scratch=None, out=None,
+            edges_only=False):
     """The whole hot path (stage 1 on Q and K, then stage 2): dense q, k, v -> (O, LSE)."""
     _dev(q, k, v)
     B, H, n_q, d = q.shape
     _, H_kv, n_kv, _ = k.shape
     desc = make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k_code, d_v=v.shape[-1], n_q=n_q, n_kv=n_kv, q_pos0=q_pos0,
-                     causal=causal, scale=scale, dtype=_dt(v), kernel=kernel)
+                     causal=causal, scale=scale, dtype=_dt(v), kernel=kernel, edges_only=edges_only)
     if scratch is None:
         scratch = torch.empty(max(scratch_bytes(desc), 16), dtype=torch.uint8, device=v.device)
     if out is None:

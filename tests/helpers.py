@@ -52,6 +52,12 @@ def assert_attn_close(o_gpu, lse_gpu, o_ref, lse_ref, dtype):
     og = o_as_f64(o_gpu, dtype)
     lg = lse_gpu.astype(np.float64)
     assert og.shape == o_ref.shape and lg.shape == lse_ref.shape
+    # rows with no allowed key / no edge (A10, R2): LSE must be -inf exactly, O exactly 0
+    dead = np.isneginf(lse_ref)
+    assert np.array_equal(np.isneginf(lg), dead), "rows with LSE = -inf differ"
+    assert np.all(og[dead] == 0.0), "rows with no allowed key must have O = 0"
+    lg = np.where(dead, 0.0, lg)
+    lse_ref = np.where(dead, 0.0, lse_ref)
     if dtype == "bf16":
         excess = np.abs(og - o_ref) - BF16_U * np.abs(o_ref)
         err_o = excess.max()
