@@ -22,6 +22,7 @@
 // Operands: codes decompressed on chip into 128B-swizzled tiles (densify.cuh), V and dO by TMA.
 #include <cudaTypedefs.h>
 #include <mutex>
+#include <type_traits>
 
 #include "densify.cuh"
 #include "launch.cuh"
@@ -33,7 +34,16 @@ using namespace dz;
 
 namespace {
 
-constexpr int BM = 128, BN = 128, NTH = 384;
+constexpr int BM = 128, BN = 128, NTH = 448;
+// Thread roles (both kernels): warps 0-7 = two groups of four row warps (TMEM lane quarter = warp & 3);
+// group g forms P / dS for the columns [64g, 64g + 64) of the 128-wide score tile, so every SMSP runs
+// two such warps (the exponentials and the TMEM traffic of one hide the latency of the other);
+// warps 8-11 decompression; warp 12 tcgen05.mma issuer + TMEM owner; warp 13 TMA.
+constexpr int ROW_WARPS = 8;
+
+// TMEM column of the packed bf16 operand (P, P^T, dS or dS^T) for the K-step kk (16 rows of K):
+// group g writes its 64 columns' worth of bf16 pairs into [64g, 64g + 32) over scores it has read
+__device__ __forceinline__ uint32_t packed_col(int kk) { return (uint32_t)(64 * (kk >> 2) + 8 * (kk & 3)); }
 
 struct BwdArgs {
     const uint8_t *q_idx, *k_idx;
@@ -83,8 +93,12 @@ struct DqCfg {
     static constexpr int OFF_BAR = OFF_V + 2 * BN * DV * 2;
     static constexpr int SMEM = OFF_BAR + 256 + 1024;
 };
+// dQ TMEM: S double-buffered in columns [0,128) / [384,512) (dS written over the buffer it came from),
+// dP [128,256), dQ~ [256,384).  S(j+1) is issued while the row warps still work on tile j; dP(j+1) as
+// soon as they have read dP(j) (DP_FREE); dQ~ += dS(j) K~(j) after that.
 enum { Q_FULL = 0, DO_FULL, K_FULL, K_EMPTY = K_FULL + 2, V_FULL = K_EMPTY + 2, V_EMPTY = V_FULL + 2, S_FULL = V_EMPTY + 2,
-       DS_READY, DQ_FULL, NBAR_DQ };
+       DP_FULL = S_FULL + 2, DP_FREE, DS_READY, DQ_FULL, NBAR_DQ };
+__device__ __forceinline__ uint32_t dq_sbuf(int j) { return (j & 1) ? 384u : 0u; }
 
 template <int D, int DV>
 __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_v,
@@ -111,11 +125,12 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NBAR_DQ; ++i)
-            mbar_init(BAR(i), (i == Q_FULL || i == K_FULL || i == K_FULL + 1 || i == DS_READY) ? 4u : 1u);
+            mbar_init(BAR(i), (i == Q_FULL || i == K_FULL || i == K_FULL + 1) ? 4u
+                              : ((i == DS_READY || i == DP_FREE) ? 8u : 1u));
         fence_mbar_init();
     }
-    if (warp == 8) tmem_alloc<512>(smem_u32(tmem_slot));
-    if (warp == 9 && lane == 0) {
+    if (warp == 12) tmem_alloc<512>(smem_u32(tmem_slot));
+    if (warp == 13 && lane == 0) {
         tma_prefetch_desc(&tm_v);
         tma_prefetch_desc(&tm_do);
     }
@@ -124,10 +139,11 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp < 4) {
-        // ==================== row warps: thread = query row = TMEM lane ====================
-        const int r = warp * 32 + lane;
-        const uint32_t lo = (uint32_t)(warp * 32) << 16;
+    if (warp < ROW_WARPS) {
+        // ==================== row warps: thread = query row = TMEM lane; group = key half ====================
+        const int grp = warp >> 2, wq = warp & 3;
+        const int r = wq * 32 + lane;
+        const uint32_t lo = (uint32_t)(wq * 32) << 16;
         const int64_t i = (int64_t)ib * BM + r;
         const bool row_ok = i < a.n_q;
         const int64_t qrow = ((int64_t)b * a.H + h) * a.n_q + i;
@@ -137,31 +153,51 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
         if (row_ok && a.causal && a.q_pos0 + i + 1 < kend) kend = a.q_pos0 + i + 1;
         const float cs = a.c_scale;
         for (int j = 0; j < nt; ++j) {
-            mbar_wait(BAR(S_FULL), j & 1);
+            const uint32_t sbuf = dq_sbuf(j);
+            mbar_wait(BAR(S_FULL + (j & 1)), (j >> 1) & 1);
+            mbar_wait(BAR(DP_FULL), j & 1);
             tc_fence_after();
             int64_t l64 = kend - (int64_t)j * BN;
             const int lim = l64 < 0 ? 0 : (l64 > BN ? BN : (int)l64);
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {  // 32 keys at a time; dS(c) overwrites S columns already read
+            for (int c = 0; c < 2; ++c) {  // 32 keys at a time; dS overwrites S columns this group has read
+                const int cc = 2 * grp + c;
                 uint32_t s[32], dp[32], pk[16];
-                tmem_ld32(tmem + lo + 32 * c, s);
-                tmem_ld32(tmem + lo + 128 + 32 * c, dp);
+                tmem_ld32(tmem + lo + sbuf + 32 * cc, s);
+                tmem_ld32(tmem + lo + 128 + 32 * cc, dp);
                 tmem_ld_wait();
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const int k0 = 32 * c + 2 * e;
-                    const float p0 = k0 < lim ? fast_exp2(fmaf(__uint_as_float(s[2 * e]), cs, -lse2)) : 0.f;
-                    const float p1 = k0 + 1 < lim ? fast_exp2(fmaf(__uint_as_float(s[2 * e + 1]), cs, -lse2)) : 0.f;
-                    pk[e] = pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - Di), p1 * (__uint_as_float(dp[2 * e + 1]) - Di));
+                if (c == 1) {  // this warp is done with dP(j): dP(j+1) may be issued
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(BAR(DP_FREE));
                 }
-                tmem_st16(tmem + lo + 16 * c, pk);
+                auto chunk = [&](auto masked) {  // masks only where the diagonal / ragged end cuts the chunk
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const int k0 = 32 * cc + 2 * e;
+                        float p0 = fast_exp2(fmaf(__uint_as_float(s[2 * e]), cs, -lse2));
+                        float p1 = fast_exp2(fmaf(__uint_as_float(s[2 * e + 1]), cs, -lse2));
+                        if (decltype(masked)::value) {
+                            if (k0 >= lim) p0 = 0.f;
+                            if (k0 + 1 >= lim) p1 = 0.f;
+                        }
+                        pk[e] = pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - Di),
+                                            p1 * (__uint_as_float(dp[2 * e + 1]) - Di));
+                    }
+                };
+                if (lim >= 32 * cc + 32)
+                    chunk(std::false_type{});
+                else
+                    chunk(std::true_type{});
+                tmem_st16(tmem + lo + sbuf + 64 * grp + 16 * c, pk);
             }
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(BAR(DS_READY));
         }
-        // ---- epilogue: dQ~ row -> shared staging (the dead K~ ring) -> gather at the support
+        if (grp == 0) {
+        // ---- epilogue (group 0): dQ~ row -> shared staging (the dead K~ ring) -> gather at the support
         mbar_wait(BAR(DQ_FULL), 0);
         tc_fence_after();
         float *st = reinterpret_cast<float *>(gb + C::OFF_K) + (size_t)r * D;
@@ -178,9 +214,10 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
                 const int f = __ldg(a.q_idx + qrow * a.k + t);
                 a.dq[qrow * a.k + t] = a.scale * st[(f + r) % D];
             }
-    } else if (warp < 8) {
+        }
+    } else if (warp < 12) {
         // ==================== decompression: Q~ once, K~ per key tile (thread = row) ====================
-        const int r = threadIdx.x - 128;
+        const int r = threadIdx.x - 32 * ROW_WARPS;
         const int k = a.k;
         {
             const int64_t i = (int64_t)ib * BM + r;
@@ -203,7 +240,7 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
             __syncwarp();
             if (lane == 0) mbar_arrive(BAR(K_FULL + s));
         }
-    } else if (warp == 8) {
+    } else if (warp == 12) {
         // ==================== tcgen05.mma issuer ====================
         if (lane == 0) {
             constexpr uint32_t idS = umma_idesc_f16kind(BM, BN, 0, 0, 1);  // Q~ . K~^T
@@ -217,7 +254,8 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
                 const uint32_t ka = sb + C::OFF_K + (jj & 1) * BN * D * 2;
 #pragma unroll
                 for (int kk = 0; kk < BN / 16; ++kk)
-                    umma_ts(tmem + 256, tmem + 8 * kk, mnmaj(ka, BN, kk), idQ, (jj > 0 || kk > 0) ? 1u : 0u);
+                    umma_ts(tmem + 256, tmem + dq_sbuf(jj) + packed_col(kk), mnmaj(ka, BN, kk), idQ,
+                            (jj > 0 || kk > 0) ? 1u : 0u);
                 umma_commit(BAR(K_EMPTY + (jj & 1)));
             };
             for (int j = 0; j < nt; ++j) {
@@ -225,21 +263,28 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
                 mbar_wait(BAR(K_FULL + s), u & 1);
                 mbar_wait(BAR(V_FULL + s), u & 1);
                 tc_fence_after();
-                if (j > 0) dq_mma(j - 1);  // in-order pipe: reads dS(j-1) before S(j) overwrites it
                 const uint32_t ka = sb + C::OFF_K + s * BN * D * 2, va = sb + C::OFF_V + s * BN * DV * 2;
+                // S(j) into the buffer of tile j-2: its dS was consumed by dQ(j-2), issued before (in order)
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) umma_ss(tmem, kmaj(qa, BM, kk), kmaj(ka, BN, kk), idS, kk > 0);
+                for (int kk = 0; kk < D / 16; ++kk)
+                    umma_ss(tmem + dq_sbuf(j), kmaj(qa, BM, kk), kmaj(ka, BN, kk), idS, kk > 0);
+                umma_commit(BAR(S_FULL + (j & 1)));
+                if (j > 0) {
+                    mbar_wait(BAR(DP_FREE), (j - 1) & 1);
+                    tc_fence_after();
+                }
 #pragma unroll
                 for (int kk = 0; kk < DV / 16; ++kk)
                     umma_ss(tmem + 128, kmaj(da, BM, kk), kmaj(va, BN, kk), idS, kk > 0);
                 umma_commit(BAR(V_EMPTY + s));
-                umma_commit(BAR(S_FULL));
+                umma_commit(BAR(DP_FULL));
+                if (j > 0) dq_mma(j - 1);
             }
             dq_mma(nt - 1);
             umma_commit(BAR(DQ_FULL));
         }
         __syncwarp();
-    } else if (warp == 9) {
+    } else if (warp == 13) {
         // ==================== TMA: dO tile once, V tiles ====================
         if (lane == 0) {
             mbar_arrive_expect_tx(BAR(DO_FULL), BM * DV * 2);
@@ -260,7 +305,7 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) {
+    if (warp == 12) {
         tc_fence_after();
         tmem_dealloc<512>(tmem);
     }
@@ -310,11 +355,11 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NBAR_KV; ++i)
-            mbar_init(BAR(i), (i == KK_FULL || i == QQ_FULL || i == QQ_FULL + 1 || i == P_READY) ? 4u : 1u);
+            mbar_init(BAR(i), (i == KK_FULL || i == QQ_FULL || i == QQ_FULL + 1) ? 4u : (i == P_READY ? 8u : 1u));
         fence_mbar_init();
     }
-    if (warp == 8) tmem_alloc<512>(smem_u32(tmem_slot));
-    if (warp == 9 && lane == 0) {
+    if (warp == 12) tmem_alloc<512>(smem_u32(tmem_slot));
+    if (warp == 13 && lane == 0) {
         tma_prefetch_desc(&tm_v);
         tma_prefetch_desc(&tm_do);
     }
@@ -324,10 +369,11 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t DV_COL = 256, DK_COL = 256 + DV;
 
-    if (warp < 4) {
-        // ==================== key warps: thread = key = TMEM lane ====================
-        const int r = warp * 32 + lane;
-        const uint32_t lo = (uint32_t)(warp * 32) << 16;
+    if (warp < ROW_WARPS) {
+        // ==================== key warps: thread = key = TMEM lane; group = query half ====================
+        const int grp = warp >> 2, wq = warp & 3;
+        const int r = wq * 32 + lane;
+        const uint32_t lo = (uint32_t)(wq * 32) << 16;
         const int64_t kj = (int64_t)jb * BN + r;
         const bool key_ok = kj < a.n_kv;
         const float cs = a.c_scale;
@@ -343,36 +389,57 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
             int64_t qmax = a.n_q - (int64_t)ib * BM;                          // one past the last valid
             if (!key_ok) qmax = 0;
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < 2; ++c) {
+                const int cc = 2 * grp + c;
                 uint32_t sv[32], dp[32], pp[16], pd[16];
-                tmem_ld32(tmem + lo + 32 * c, sv);
-                tmem_ld32(tmem + lo + 128 + 32 * c, dp);
+                tmem_ld32(tmem + lo + 32 * cc, sv);
+                tmem_ld32(tmem + lo + 128 + 32 * cc, dp);
                 tmem_ld_wait();
+                // LSE and D of 4 queries per 16-byte shared load; the mask tests only on chunks the
+                // causal diagonal or the ragged end cuts (most steps have every pair allowed)
+                auto chunk = [&](auto masked) {
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    const int q0 = 32 * c + 2 * e;
-                    const bool a0 = q0 >= qmin && q0 < qmax, a1 = q0 + 1 >= qmin && q0 + 1 < qmax;
-                    const float p0 = a0 ? fast_exp2(fmaf(__uint_as_float(sv[2 * e]), cs, -lse2[q0])) : 0.f;
-                    const float p1 = a1 ? fast_exp2(fmaf(__uint_as_float(sv[2 * e + 1]), cs, -lse2[q0 + 1])) : 0.f;
-                    pp[e] = pack_bf16x2(p0, p1);
-                    pd[e] = pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - Dq[q0]),
-                                        p1 * (__uint_as_float(dp[2 * e + 1]) - Dq[q0 + 1]));
-                }
-                tmem_st16(tmem + lo + 16 * c, pp);        // P^T over S^T's columns already read
-                tmem_st16(tmem + lo + 128 + 16 * c, pd);  // dS^T over dP^T's
+                    for (int e4 = 0; e4 < 8; ++e4) {
+                        const int qb = 32 * cc + 4 * e4;
+                        const float4 L = *reinterpret_cast<const float4 *>(lse2 + qb);
+                        const float4 Dv = *reinterpret_cast<const float4 *>(Dq + qb);
+                        const float lv[4] = {L.x, L.y, L.z, L.w}, dv[4] = {Dv.x, Dv.y, Dv.z, Dv.w};
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int e = 2 * e4 + h, q0 = qb + 2 * h;
+                            float p0 = fast_exp2(fmaf(__uint_as_float(sv[2 * e]), cs, -lv[2 * h]));
+                            float p1 = fast_exp2(fmaf(__uint_as_float(sv[2 * e + 1]), cs, -lv[2 * h + 1]));
+                            if (decltype(masked)::value) {
+                                if (!(q0 >= qmin && q0 < qmax)) p0 = 0.f;
+                                if (!(q0 + 1 >= qmin && q0 + 1 < qmax)) p1 = 0.f;
+                            }
+                            pp[e] = pack_bf16x2(p0, p1);
+                            pd[e] = pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - dv[2 * h]),
+                                                p1 * (__uint_as_float(dp[2 * e + 1]) - dv[2 * h + 1]));
+                        }
+                    }
+                };
+                if (qmin <= 32 * cc && qmax >= 32 * cc + 32)
+                    chunk(std::false_type{});
+                else
+                    chunk(std::true_type{});
+                tmem_st16(tmem + lo + 64 * grp + 16 * c, pp);        // P^T over S^T columns this group read
+                tmem_st16(tmem + lo + 128 + 64 * grp + 16 * c, pd);  // dS^T over dP^T's
             }
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(BAR(P_READY));
         }
-        // ---- epilogue: dV row (fp32) straight out; dK~ row -> staging (dead Q~ ring) -> support gather
+        // ---- epilogue: group 0 writes the dV row (fp32) straight out; group 1 stages the dK~ row
+        // (dead Q~ ring) and gathers it at the support
         const int64_t krow = ((int64_t)b * a.H_kv + g) * a.n_kv + kj;
         float *stg = reinterpret_cast<float *>(gb + C::OFF_Q) + (size_t)r * D;
         if (ns > 0) {
             mbar_wait(BAR(OUT_FULL), 0);
             tc_fence_after();
         }
+        if (grp == 0) {
 #pragma unroll 1
         for (int c = 0; c < DV / 32; ++c) {
             uint32_t o[32];
@@ -391,6 +458,7 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
                                           __uint_as_float(o[4 * v4 + 2]), __uint_as_float(o[4 * v4 + 3]));
             }
         }
+        } else {
 #pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
             uint32_t o[32];
@@ -409,9 +477,10 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
                 const int f = __ldg(a.k_idx + krow * a.k + t);
                 a.dk[krow * a.k + t] = a.scale * stg[(f + r) % D];
             }
-    } else if (warp < 8) {
+        }
+    } else if (warp < 12) {
         // ==================== decompression: K~ once, Q~ (+ LSE, D) per step (thread = row) ====================
-        const int r = threadIdx.x - 128;
+        const int r = threadIdx.x - 32 * ROW_WARPS;
         const int k = a.k;
         const int64_t kv0 = ((int64_t)b * a.H_kv + g) * a.n_kv;
         {
@@ -437,7 +506,7 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
             __syncwarp();
             if (lane == 0) mbar_arrive(BAR(QQ_FULL + st));
         }
-    } else if (warp == 8) {
+    } else if (warp == 12) {
         // ==================== tcgen05.mma issuer ====================
         if (lane == 0 && ns > 0) {
             constexpr uint32_t idS = umma_idesc_f16kind(BN, BM, 0, 0, 1);  // K~ . Q~^T and V . dO^T
@@ -453,10 +522,11 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
                 const uint32_t qa = sb + C::OFF_Q + st * BM * D * 2, da = sb + C::OFF_DO + st * BM * DV * 2;
 #pragma unroll
                 for (int kk = 0; kk < BM / 16; ++kk)
-                    umma_ts(tmem + DV_COL, tmem + 8 * kk, mnmaj(da, BM, kk), idV, (ss > 0 || kk > 0) ? 1u : 0u);
+                    umma_ts(tmem + DV_COL, tmem + packed_col(kk), mnmaj(da, BM, kk), idV, (ss > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
                 for (int kk = 0; kk < BM / 16; ++kk)
-                    umma_ts(tmem + DK_COL, tmem + 128 + 8 * kk, mnmaj(qa, BM, kk), idK, (ss > 0 || kk > 0) ? 1u : 0u);
+                    umma_ts(tmem + DK_COL, tmem + 128 + packed_col(kk), mnmaj(qa, BM, kk), idK,
+                            (ss > 0 || kk > 0) ? 1u : 0u);
                 umma_commit(BAR(QQ_EMPTY + st));
                 umma_commit(BAR(DOO_EMPTY + st));
             };
@@ -478,7 +548,7 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
             umma_commit(BAR(OUT_FULL));
         }
         __syncwarp();
-    } else if (warp == 9) {
+    } else if (warp == 13) {
         // ==================== TMA: V tile once, dO tiles per step ====================
         if (lane == 0 && ns > 0) {
             mbar_arrive_expect_tx(BAR(KV_FULL), BN * DV * 2);
@@ -500,7 +570,7 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) {
+    if (warp == 12) {
         tc_fence_after();
         tmem_dealloc<512>(tmem);
     }
