@@ -234,6 +234,7 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
             const int64_t key = (int64_t)j * BN + r;
             const bool ok = key < a.n_kv;
             const int64_t kr = kv0 + (ok ? key : 0);
+            if (j + 1 < nt && key + BN < a.n_kv) prefetch_code_row(a.k_idx + (kr + BN) * k, a.k_val + (kr + BN) * k);
             mbar_wait(BAR(K_EMPTY + s), (u & 1) ^ 1);
             densify_row<D>(sb + C::OFF_K + s * BN * D * 2, BN, r, ok, a.k_idx + kr * k, a.k_val + kr * k, k);
             fence_proxy_async_smem();
@@ -325,8 +326,14 @@ struct KvCfg {
     static constexpr int OFF_BAR = OFF_LD + 2 * 2 * BM * 4;
     static constexpr int SMEM = OFF_BAR + 256 + 1024;
 };
+// dK~/dV pipeline per step s (TMEM: S^T [0,128) | dP^T [128,256) | dV | dK~, all 512 columns):
+//   MMA:   ... [P_READY(s)] dV += P^T(s) dO(s);  S^T(s+1)  [KDS_READY(s)] dK~ += dS^T(s) Q~(s);  dP^T(s+1)
+//   warps: [SS_FULL] P-phase (P^T(s) over S^T) -> P_READY;  [KDP_FULL] dS-phase (dS^T over dP^T) -> KDS_READY
+// S^T(s+1) overwrites P^T(s) and dP^T(s+1) overwrites dS^T(s) only after the MMAs reading them were
+// issued (in-order tensor pipe), so the warps' dS-phase of step s overlaps S^T(s+1) and dV(s), and
+// their P-phase of step s+1 overlaps dK~(s) and dP^T(s+1).
 enum { KK_FULL = 0, KV_FULL, QQ_FULL, QQ_EMPTY = QQ_FULL + 2, DOO_FULL = QQ_EMPTY + 2, DOO_EMPTY = DOO_FULL + 2,
-       SS_FULL = DOO_EMPTY + 2, P_READY, OUT_FULL, NBAR_KV };
+       SS_FULL = DOO_EMPTY + 2, KDP_FULL, P_READY, KDS_READY, OUT_FULL, NBAR_KV };
 
 template <int D, int DV>
 __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_v,
@@ -355,7 +362,8 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NBAR_KV; ++i)
-            mbar_init(BAR(i), (i == KK_FULL || i == QQ_FULL || i == QQ_FULL + 1) ? 4u : (i == P_READY ? 8u : 1u));
+            mbar_init(BAR(i), (i == KK_FULL || i == QQ_FULL || i == QQ_FULL + 1) ? 4u
+                              : ((i == P_READY || i == KDS_READY) ? 8u : 1u));
         fence_mbar_init();
     }
     if (warp == 12) tmem_alloc<512>(smem_u32(tmem_slot));
@@ -388,48 +396,65 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
             if (qmin < 0) qmin = 0;
             int64_t qmax = a.n_q - (int64_t)ib * BM;                          // one past the last valid
             if (!key_ok) qmax = 0;
-#pragma unroll 1
+            // P-phase: p from S^T and LSE (kept in fp32 for the dS-phase), P^T in bf16 over S^T
+            float pk[2][32];
+#pragma unroll
             for (int c = 0; c < 2; ++c) {
                 const int cc = 2 * grp + c;
-                uint32_t sv[32], dp[32], pp[16], pd[16];
+                uint32_t sv[32], pp[16];
                 tmem_ld32(tmem + lo + 32 * cc, sv);
-                tmem_ld32(tmem + lo + 128 + 32 * cc, dp);
                 tmem_ld_wait();
-                // LSE and D of 4 queries per 16-byte shared load; the mask tests only on chunks the
-                // causal diagonal or the ragged end cuts (most steps have every pair allowed)
-                auto chunk = [&](auto masked) {
+                // LSE of 4 queries per 16-byte shared load; the mask tests only on chunks the causal
+                // diagonal or the ragged end cuts (most steps have every pair allowed)
+                auto pchunk = [&](auto masked) {
 #pragma unroll
                     for (int e4 = 0; e4 < 8; ++e4) {
                         const int qb = 32 * cc + 4 * e4;
                         const float4 L = *reinterpret_cast<const float4 *>(lse2 + qb);
-                        const float4 Dv = *reinterpret_cast<const float4 *>(Dq + qb);
-                        const float lv[4] = {L.x, L.y, L.z, L.w}, dv[4] = {Dv.x, Dv.y, Dv.z, Dv.w};
+                        const float lv[4] = {L.x, L.y, L.z, L.w};
 #pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int e = 2 * e4 + h, q0 = qb + 2 * h;
-                            float p0 = fast_exp2(fmaf(__uint_as_float(sv[2 * e]), cs, -lv[2 * h]));
-                            float p1 = fast_exp2(fmaf(__uint_as_float(sv[2 * e + 1]), cs, -lv[2 * h + 1]));
-                            if (decltype(masked)::value) {
-                                if (!(q0 >= qmin && q0 < qmax)) p0 = 0.f;
-                                if (!(q0 + 1 >= qmin && q0 + 1 < qmax)) p1 = 0.f;
-                            }
-                            pp[e] = pack_bf16x2(p0, p1);
-                            pd[e] = pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - dv[2 * h]),
-                                                p1 * (__uint_as_float(dp[2 * e + 1]) - dv[2 * h + 1]));
+                        for (int u = 0; u < 4; ++u) {
+                            float p = fast_exp2(fmaf(__uint_as_float(sv[4 * e4 + u]), cs, -lv[u]));
+                            if (decltype(masked)::value && !(qb + u >= qmin && qb + u < qmax)) p = 0.f;
+                            pk[c][4 * e4 + u] = p;
                         }
                     }
                 };
                 if (qmin <= 32 * cc && qmax >= 32 * cc + 32)
-                    chunk(std::false_type{});
+                    pchunk(std::false_type{});
                 else
-                    chunk(std::true_type{});
-                tmem_st16(tmem + lo + 64 * grp + 16 * c, pp);        // P^T over S^T columns this group read
-                tmem_st16(tmem + lo + 128 + 64 * grp + 16 * c, pd);  // dS^T over dP^T's
+                    pchunk(std::true_type{});
+#pragma unroll
+                for (int e = 0; e < 16; ++e) pp[e] = pack_bf16x2(pk[c][2 * e], pk[c][2 * e + 1]);
+                tmem_st16(tmem + lo + 64 * grp + 16 * c, pp);  // P^T over S^T columns this group read
             }
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(BAR(P_READY));
+            // dS-phase: dS^T = P^T (.) (dP^T - D), bf16 over dP^T
+            mbar_wait(BAR(KDP_FULL), s & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int cc = 2 * grp + c;
+                uint32_t dp[32], pd[16];
+                tmem_ld32(tmem + lo + 128 + 32 * cc, dp);
+                tmem_ld_wait();
+#pragma unroll
+                for (int e4 = 0; e4 < 8; ++e4) {
+                    const float4 Dv = *reinterpret_cast<const float4 *>(Dq + 32 * cc + 4 * e4);
+                    pd[2 * e4] = pack_bf16x2(pk[c][4 * e4] * (__uint_as_float(dp[4 * e4]) - Dv.x),
+                                             pk[c][4 * e4 + 1] * (__uint_as_float(dp[4 * e4 + 1]) - Dv.y));
+                    pd[2 * e4 + 1] = pack_bf16x2(pk[c][4 * e4 + 2] * (__uint_as_float(dp[4 * e4 + 2]) - Dv.z),
+                                                 pk[c][4 * e4 + 3] * (__uint_as_float(dp[4 * e4 + 3]) - Dv.w));
+                }
+                tmem_st16(tmem + lo + 128 + 64 * grp + 16 * c, pd);  // dS^T over dP^T's
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(BAR(KDS_READY));
         }
         // ---- epilogue: group 0 writes the dV row (fp32) straight out; group 1 stages the dK~ row
         // (dead Q~ ring) and gathers it at the support
@@ -498,6 +523,14 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
             const int64_t i = (int64_t)ib * BM + r;
             const bool ok = i < a.n_q;
             const int64_t row = ((int64_t)b * a.H + h) * a.n_q + (ok ? i : 0);
+            if (s + 1 < ns) {  // next step's query codes (and LSE, D) into L1
+                const int h1 = g * R + (s + 1) / nib, ib1 = ib0 + (s + 1) % nib;
+                const int64_t i1 = (int64_t)ib1 * BM + r;
+                if (i1 < a.n_q) {
+                    const int64_t row1 = ((int64_t)b * a.H + h1) * a.n_q + i1;
+                    prefetch_code_row(a.q_idx + row1 * k, a.q_val + row1 * k);
+                }
+            }
             mbar_wait(BAR(QQ_EMPTY + st), (u & 1) ^ 1);
             densify_row<D>(sb + C::OFF_Q + st * BM * D * 2, BM, r, ok, a.q_idx + row * k, a.q_val + row * k, k);
             ldv[st * 2 * BM + r] = ok ? __ldg(a.lse + row) * 1.4426950408889634f : 0.f;
@@ -515,36 +548,48 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
             const uint32_t ka = sb + C::OFF_K, va = sb + C::OFF_V;
             mbar_wait(BAR(KK_FULL), 0);
             mbar_wait(BAR(KV_FULL), 0);
-            auto grad_mma = [&](int ss) {  // dV += P^T(ss) dO(ss), dK~ += dS^T(ss) Q~(ss)
-                const int st = ss & 1;
-                mbar_wait(BAR(P_READY), ss & 1);
-                tc_fence_after();
-                const uint32_t qa = sb + C::OFF_Q + st * BM * D * 2, da = sb + C::OFF_DO + st * BM * DV * 2;
-#pragma unroll
-                for (int kk = 0; kk < BM / 16; ++kk)
-                    umma_ts(tmem + DV_COL, tmem + packed_col(kk), mnmaj(da, BM, kk), idV, (ss > 0 || kk > 0) ? 1u : 0u);
-#pragma unroll
-                for (int kk = 0; kk < BM / 16; ++kk)
-                    umma_ts(tmem + DK_COL, tmem + 128 + packed_col(kk), mnmaj(qa, BM, kk), idK,
-                            (ss > 0 || kk > 0) ? 1u : 0u);
-                umma_commit(BAR(QQ_EMPTY + st));
-                umma_commit(BAR(DOO_EMPTY + st));
-            };
-            for (int s = 0; s < ns; ++s) {
-                const int st = s & 1, u = s >> 1;
-                mbar_wait(BAR(QQ_FULL + st), u & 1);
-                mbar_wait(BAR(DOO_FULL + st), u & 1);
-                tc_fence_after();
-                if (s > 0) grad_mma(s - 1);  // in-order pipe: reads P^T/dS^T(s-1) before S^T(s) lands
-                const uint32_t qa = sb + C::OFF_Q + st * BM * D * 2, da = sb + C::OFF_DO + st * BM * DV * 2;
+            auto issue_S = [&](int ss) {  // S^T = K~ Q~(ss)^T
+                const uint32_t qa = sb + C::OFF_Q + (ss & 1) * BM * D * 2;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) umma_ss(tmem, kmaj(ka, BN, kk), kmaj(qa, BM, kk), idS, kk > 0);
-#pragma unroll
-                for (int kk = 0; kk < DV / 16; ++kk)
-                    umma_ss(tmem + 128, kmaj(va, BN, kk), kmaj(da, BM, kk), idS, kk > 0);
                 umma_commit(BAR(SS_FULL));
+            };
+            auto issue_dP = [&](int ss) {  // dP^T = V dO(ss)^T
+                const uint32_t da = sb + C::OFF_DO + (ss & 1) * BM * DV * 2;
+#pragma unroll
+                for (int kk = 0; kk < DV / 16; ++kk) umma_ss(tmem + 128, kmaj(va, BN, kk), kmaj(da, BM, kk), idS, kk > 0);
+                umma_commit(BAR(KDP_FULL));
+            };
+            mbar_wait(BAR(QQ_FULL), 0);
+            mbar_wait(BAR(DOO_FULL), 0);
+            tc_fence_after();
+            issue_S(0);
+            issue_dP(0);
+            for (int s = 0; s < ns; ++s) {
+                const int st = s & 1;
+                const uint32_t qa = sb + C::OFF_Q + st * BM * D * 2, da = sb + C::OFF_DO + st * BM * DV * 2;
+                mbar_wait(BAR(P_READY), s & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < BM / 16; ++kk)  // dV += P^T dO
+                    umma_ts(tmem + DV_COL, tmem + packed_col(kk), mnmaj(da, BM, kk), idV, (s > 0 || kk > 0) ? 1u : 0u);
+                umma_commit(BAR(DOO_EMPTY + st));
+                if (s + 1 < ns) {
+                    const int s1 = s + 1;
+                    mbar_wait(BAR(QQ_FULL + (s1 & 1)), (s1 >> 1) & 1);
+                    mbar_wait(BAR(DOO_FULL + (s1 & 1)), (s1 >> 1) & 1);
+                    tc_fence_after();
+                    issue_S(s1);  // over P^T(s): dV(s), issued above, reads it first
+                }
+                mbar_wait(BAR(KDS_READY), s & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int kk = 0; kk < BM / 16; ++kk)  // dK~ += dS^T Q~
+                    umma_ts(tmem + DK_COL, tmem + 128 + packed_col(kk), mnmaj(qa, BM, kk), idK,
+                            (s > 0 || kk > 0) ? 1u : 0u);
+                umma_commit(BAR(QQ_EMPTY + st));
+                if (s + 1 < ns) issue_dP(s + 1);  // over dS^T(s): dK~(s), issued above, reads it first
             }
-            grad_mma(ns - 1);
             umma_commit(BAR(OUT_FULL));
         }
         __syncwarp();

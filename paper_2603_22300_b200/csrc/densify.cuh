@@ -18,6 +18,13 @@ __device__ __forceinline__ void sts_u16(uint32_t addr, uint32_t v) {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((uint16_t)v) : "memory");
 }
 
+// the code row (idx, val) a later densify_row will read: into L1 ahead of time (issued one tile early,
+// so the decompression after the ring slot frees does not wait on L2)
+__device__ __forceinline__ void prefetch_code_row(const uint8_t *idx, const uint16_t *val) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(idx));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(val));
+}
+
 // zero row r of a swizzled tile (D features) then write its k code values
 template <int D>
 __device__ __forceinline__ void densify_row(uint32_t tile, int rows, int r, bool valid, const uint8_t *__restrict__ idx,
