@@ -88,15 +88,17 @@ template <int D, int DV>
 struct DqCfg {
     static constexpr int OFF_Q = 0;                      // Q~ tile  [128][D] bf16
     static constexpr int OFF_DO = OFF_Q + BM * D * 2;    // dO tile  [128][DV] bf16
-    static constexpr int OFF_K = OFF_DO + BM * DV * 2;   // K~ ring  2 x [128][D]
-    static constexpr int OFF_V = OFF_K + 2 * BN * D * 2; // V ring   2 x [128][DV]
+    static constexpr int NK = 3;                          // K~ ring depth (K~(j+2) decompresses while dQ(j) waits)
+    static constexpr int OFF_K = OFF_DO + BM * DV * 2;    // K~ ring  NK x [128][D]
+    static constexpr int OFF_V = OFF_K + NK * BN * D * 2; // V ring   2 x [128][DV]
     static constexpr int OFF_BAR = OFF_V + 2 * BN * DV * 2;
     static constexpr int SMEM = OFF_BAR + 256 + 1024;
 };
+static_assert(DqCfg<128, 128>::SMEM <= 232448, "dQ kernel shared memory");
 // dQ TMEM: S double-buffered in columns [0,128) / [384,512) (dS written over the buffer it came from),
 // dP [128,256), dQ~ [256,384).  S(j+1) is issued while the row warps still work on tile j; dP(j+1) as
 // soon as they have read dP(j) (DP_FREE); dQ~ += dS(j) K~(j) after that.
-enum { Q_FULL = 0, DO_FULL, K_FULL, K_EMPTY = K_FULL + 2, V_FULL = K_EMPTY + 2, V_EMPTY = V_FULL + 2, S_FULL = V_EMPTY + 2,
+enum { Q_FULL = 0, DO_FULL, K_FULL, K_EMPTY = K_FULL + 3, V_FULL = K_EMPTY + 3, V_EMPTY = V_FULL + 2, S_FULL = V_EMPTY + 2,
        DP_FULL = S_FULL + 2, DP_FREE, DS_READY, DQ_FULL, NBAR_DQ };
 __device__ __forceinline__ uint32_t dq_sbuf(int j) { return (j & 1) ? 384u : 0u; }
 
@@ -125,7 +127,7 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NBAR_DQ; ++i)
-            mbar_init(BAR(i), (i == Q_FULL || i == K_FULL || i == K_FULL + 1) ? 4u
+            mbar_init(BAR(i), (i == Q_FULL || i == K_FULL || i == K_FULL + 1 || i == K_FULL + 2) ? 4u
                               : ((i == DS_READY || i == DP_FREE) ? 8u : 1u));
         fence_mbar_init();
     }
@@ -230,7 +232,7 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
         if (lane == 0) mbar_arrive(BAR(Q_FULL));
         const int64_t kv0 = ((int64_t)b * a.H_kv + g) * a.n_kv;
         for (int j = 0; j < nt; ++j) {
-            const int s = j & 1, u = j >> 1;
+            const int s = j % C::NK, u = j / C::NK;
             const int64_t key = (int64_t)j * BN + r;
             const bool ok = key < a.n_kv;
             const int64_t kr = kv0 + (ok ? key : 0);
@@ -252,28 +254,26 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
             auto dq_mma = [&](int jj) {  // dQ~ += dS(jj) K~(jj)
                 mbar_wait(BAR(DS_READY), jj & 1);
                 tc_fence_after();
-                const uint32_t ka = sb + C::OFF_K + (jj & 1) * BN * D * 2;
+                const uint32_t ka = sb + C::OFF_K + (jj % C::NK) * BN * D * 2;
 #pragma unroll
                 for (int kk = 0; kk < BN / 16; ++kk)
                     umma_ts(tmem + 256, tmem + dq_sbuf(jj) + packed_col(kk), mnmaj(ka, BN, kk), idQ,
                             (jj > 0 || kk > 0) ? 1u : 0u);
-                umma_commit(BAR(K_EMPTY + (jj & 1)));
+                umma_commit(BAR(K_EMPTY + jj % C::NK));
             };
             for (int j = 0; j < nt; ++j) {
-                const int s = j & 1, u = j >> 1;
-                mbar_wait(BAR(K_FULL + s), u & 1);
-                mbar_wait(BAR(V_FULL + s), u & 1);
+                const int s = j & 1, u = j >> 1, sk = j % C::NK;
+                mbar_wait(BAR(K_FULL + sk), (j / C::NK) & 1);
                 tc_fence_after();
-                const uint32_t ka = sb + C::OFF_K + s * BN * D * 2, va = sb + C::OFF_V + s * BN * DV * 2;
+                const uint32_t ka = sb + C::OFF_K + sk * BN * D * 2, va = sb + C::OFF_V + s * BN * DV * 2;
                 // S(j) into the buffer of tile j-2: its dS was consumed by dQ(j-2), issued before (in order)
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk)
                     umma_ss(tmem + dq_sbuf(j), kmaj(qa, BM, kk), kmaj(ka, BN, kk), idS, kk > 0);
                 umma_commit(BAR(S_FULL + (j & 1)));
-                if (j > 0) {
-                    mbar_wait(BAR(DP_FREE), (j - 1) & 1);
-                    tc_fence_after();
-                }
+                mbar_wait(BAR(V_FULL + s), u & 1);
+                if (j > 0) mbar_wait(BAR(DP_FREE), (j - 1) & 1);
+                tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < DV / 16; ++kk)
                     umma_ss(tmem + 128, kmaj(da, BM, kk), kmaj(va, BN, kk), idS, kk > 0);
@@ -320,20 +320,24 @@ template <int D, int DV>
 struct KvCfg {
     static constexpr int OFF_K = 0;                        // K~ tile [128][D]
     static constexpr int OFF_V = OFF_K + BN * D * 2;       // V tile  [128][DV]
-    static constexpr int OFF_Q = OFF_V + BN * DV * 2;      // Q~ ring 2 x [128][D]
-    static constexpr int OFF_DO = OFF_Q + 2 * BM * D * 2;  // dO ring 2 x [128][DV]
-    static constexpr int OFF_LD = OFF_DO + 2 * BM * DV * 2; // 2 stages x {LSE*log2e, D} x 128 fp32
-    static constexpr int OFF_BAR = OFF_LD + 2 * 2 * BM * 4;
+    static constexpr int NQ = 3;                           // Q~ (+ LSE, D) ring depth
+    static constexpr int OFF_Q = OFF_V + BN * DV * 2;      // Q~ ring NQ x [128][D]
+    static constexpr int OFF_DO = OFF_Q + NQ * BM * D * 2; // dO tile [128][DV] (single stage)
+    static constexpr int OFF_LD = OFF_DO + BM * DV * 2;    // NQ stages x {LSE*log2e, D} x 128 fp32
+    static constexpr int OFF_BAR = OFF_LD + NQ * 2 * BM * 4;
     static constexpr int SMEM = OFF_BAR + 256 + 1024;
 };
+static_assert(KvCfg<128, 128>::SMEM <= 232448, "dK/dV kernel shared memory");
 // dK~/dV pipeline per step s (TMEM: S^T [0,128) | dP^T [128,256) | dV | dK~, all 512 columns):
 //   MMA:   ... [P_READY(s)] dV += P^T(s) dO(s);  S^T(s+1)  [KDS_READY(s)] dK~ += dS^T(s) Q~(s);  dP^T(s+1)
 //   warps: [SS_FULL] P-phase (P^T(s) over S^T) -> P_READY;  [KDP_FULL] dS-phase (dS^T over dP^T) -> KDS_READY
 // S^T(s+1) overwrites P^T(s) and dP^T(s+1) overwrites dS^T(s) only after the MMAs reading them were
 // issued (in-order tensor pipe), so the warps' dS-phase of step s overlaps S^T(s+1) and dV(s), and
 // their P-phase of step s+1 overlaps dK~(s) and dP^T(s+1).
-enum { KK_FULL = 0, KV_FULL, QQ_FULL, QQ_EMPTY = QQ_FULL + 2, DOO_FULL = QQ_EMPTY + 2, DOO_EMPTY = DOO_FULL + 2,
-       SS_FULL = DOO_EMPTY + 2, KDP_FULL, P_READY, KDS_READY, OUT_FULL, NBAR_KV };
+// Q~ ring of 3: Q~(s+1) lands in the slot dK~(s-2) released, so its decompression is off the
+// S^T(s+1) critical path; dO needs one stage (dP^T(s+1) is issued well after dV(s) frees it).
+enum { KK_FULL = 0, KV_FULL, QQ_FULL, QQ_EMPTY = QQ_FULL + 3, DOO_FULL = QQ_EMPTY + 3, DOO_EMPTY,
+       SS_FULL, KDP_FULL, P_READY, KDS_READY, OUT_FULL, NBAR_KV };
 
 template <int D, int DV>
 __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_v,
@@ -362,7 +366,7 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NBAR_KV; ++i)
-            mbar_init(BAR(i), (i == KK_FULL || i == QQ_FULL || i == QQ_FULL + 1) ? 4u
+            mbar_init(BAR(i), (i == KK_FULL || i == QQ_FULL || i == QQ_FULL + 1 || i == QQ_FULL + 2) ? 4u
                               : ((i == P_READY || i == KDS_READY) ? 8u : 1u));
         fence_mbar_init();
     }
@@ -386,9 +390,9 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
         const bool key_ok = kj < a.n_kv;
         const float cs = a.c_scale;
         for (int s = 0; s < ns; ++s) {
-            const int st = s & 1, ib = ib0 + s % nib;
+            const int st = s % C::NQ, ib = ib0 + s % nib;
             mbar_wait(BAR(SS_FULL), s & 1);
-            mbar_wait(BAR(QQ_FULL + st), (s >> 1) & 1);  // LSE / D of this step visible (generic stores)
+            mbar_wait(BAR(QQ_FULL + st), (s / C::NQ) & 1);  // LSE / D of this step visible (generic stores)
             tc_fence_after();
             const float *lse2 = ldv + st * 2 * BM, *Dq = lse2 + BM;
             // query q of this tile may use key kj iff q < n_q and (non-causal or kj <= q_pos0 + q)
@@ -518,7 +522,7 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
         __syncwarp();
         if (lane == 0) mbar_arrive(BAR(KK_FULL));
         for (int s = 0; s < ns; ++s) {
-            const int st = s & 1, u = s >> 1;
+            const int st = s % C::NQ, u = s / C::NQ;
             const int h = g * R + s / nib, ib = ib0 + s % nib;
             const int64_t i = (int64_t)ib * BM + r;
             const bool ok = i < a.n_q;
@@ -549,35 +553,35 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
             mbar_wait(BAR(KK_FULL), 0);
             mbar_wait(BAR(KV_FULL), 0);
             auto issue_S = [&](int ss) {  // S^T = K~ Q~(ss)^T
-                const uint32_t qa = sb + C::OFF_Q + (ss & 1) * BM * D * 2;
+                const uint32_t qa = sb + C::OFF_Q + (ss % C::NQ) * BM * D * 2;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) umma_ss(tmem, kmaj(ka, BN, kk), kmaj(qa, BM, kk), idS, kk > 0);
                 umma_commit(BAR(SS_FULL));
             };
             auto issue_dP = [&](int ss) {  // dP^T = V dO(ss)^T
-                const uint32_t da = sb + C::OFF_DO + (ss & 1) * BM * DV * 2;
+                const uint32_t da = sb + C::OFF_DO;
+                mbar_wait(BAR(DOO_FULL), ss & 1);
+                tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < DV / 16; ++kk) umma_ss(tmem + 128, kmaj(va, BN, kk), kmaj(da, BM, kk), idS, kk > 0);
                 umma_commit(BAR(KDP_FULL));
             };
             mbar_wait(BAR(QQ_FULL), 0);
-            mbar_wait(BAR(DOO_FULL), 0);
             tc_fence_after();
             issue_S(0);
             issue_dP(0);
             for (int s = 0; s < ns; ++s) {
-                const int st = s & 1;
-                const uint32_t qa = sb + C::OFF_Q + st * BM * D * 2, da = sb + C::OFF_DO + st * BM * DV * 2;
+                const int st = s % C::NQ;
+                const uint32_t qa = sb + C::OFF_Q + st * BM * D * 2, da = sb + C::OFF_DO;
                 mbar_wait(BAR(P_READY), s & 1);
                 tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < BM / 16; ++kk)  // dV += P^T dO
                     umma_ts(tmem + DV_COL, tmem + packed_col(kk), mnmaj(da, BM, kk), idV, (s > 0 || kk > 0) ? 1u : 0u);
-                umma_commit(BAR(DOO_EMPTY + st));
+                umma_commit(BAR(DOO_EMPTY));
                 if (s + 1 < ns) {
                     const int s1 = s + 1;
-                    mbar_wait(BAR(QQ_FULL + (s1 & 1)), (s1 >> 1) & 1);
-                    mbar_wait(BAR(DOO_FULL + (s1 & 1)), (s1 >> 1) & 1);
+                    mbar_wait(BAR(QQ_FULL + s1 % C::NQ), (s1 / C::NQ) & 1);
                     tc_fence_after();
                     issue_S(s1);  // over P^T(s): dV(s), issued above, reads it first
                 }
@@ -601,14 +605,12 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
             for (int cb = 0; cb < DV / 64; ++cb)
                 tma_load_3d(sb + C::OFF_V + cb * BN * 128, &tm_v, BAR(KV_FULL), cb * 64, jb * BN, b * a.H_kv + g);
             for (int s = 0; s < ns; ++s) {
-                const int st = s & 1, u = s >> 1;
                 const int h = g * R + s / nib, ib = ib0 + s % nib;
-                mbar_wait(BAR(DOO_EMPTY + st), (u & 1) ^ 1);
-                mbar_arrive_expect_tx(BAR(DOO_FULL + st), BM * DV * 2);
+                mbar_wait(BAR(DOO_EMPTY), (s & 1) ^ 1);
+                mbar_arrive_expect_tx(BAR(DOO_FULL), BM * DV * 2);
 #pragma unroll
                 for (int cb = 0; cb < DV / 64; ++cb)
-                    tma_load_3d(sb + C::OFF_DO + st * BM * DV * 2 + cb * BM * 128, &tm_do, BAR(DOO_FULL + st), cb * 64,
-                                ib * BM, b * a.H + h);
+                    tma_load_3d(sb + C::OFF_DO + cb * BM * 128, &tm_do, BAR(DOO_FULL), cb * 64, ib * BM, b * a.H + h);
             }
         }
         __syncwarp();
