@@ -47,6 +47,9 @@ struct DecArgs {
     int64_t chunk;
 };
 
+#ifndef SFA_DEC_WAVES
+#define SFA_DEC_WAVES 4
+#endif
 constexpr int DB = 256;  // keys per V block streamed by the producer
 constexpr int NST = 3;   // V ring stages
 
@@ -196,27 +199,27 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) decode_partial_kernel(const D
                     for (int r = 0; r < ROWS; ++r) sc[r] = fmaf(qs[f * ROWS + r], kvf, sc[r]);
                 }
             }
-            // ---- steps 5-6: mask + online softmax per row (warp-wide block max and sum)
+            // ---- steps 5-6: mask + online softmax per row.  The block max is one redux.sync.max.f32
+            // (warp-uniform, so the rescale branch is uniform and taken only when the max grows); the
+            // row sum l stays a per-lane partial (same reference max in every lane), summed once at the end.
             float p[ROWS];
 #pragma unroll
             for (int r = 0; r < ROWS; ++r) {
                 bool ok = kval && r < rows;
                 if (ok && a.causal) ok = key <= a.q_pos0 + (r % (int)a.n_q);
                 const float x = ok ? sc[r] : -INFINITY;
-                float bm = x;
+                float bm;
+                asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(bm) : "f"(x));
+                if (bm > m[r]) {
+                    const float alpha = fast_exp2(m[r] - bm);  // m = -inf -> 0
+                    l[r] *= alpha;
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
-                const float mn = fmaxf(m[r], bm);
-                const float ms = mn == -INFINITY ? 0.f : mn;
-                const float alpha = fast_exp2(m[r] - ms);
+                    for (int e = 0; e < DPL; ++e) acc[r][e] *= alpha;
+                    m[r] = bm;
+                }
+                const float ms = m[r] == -INFINITY ? 0.f : m[r];
                 p[r] = ok ? fast_exp2(x - ms) : 0.f;
-                float ps = p[r];
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
-                l[r] = l[r] * alpha + ps;
-#pragma unroll
-                for (int e = 0; e < DPL; ++e) acc[r][e] *= alpha;
-                m[r] = mn;
+                l[r] += p[r];
             }
             // ---- step 7: O += p V over this warp's 32 keys, V from the ring, p from shared memory
             float *pw = pbuf + warp * 32 * ROWS;
@@ -267,9 +270,12 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) decode_partial_kernel(const D
     if (warp < CW) {
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
+            float ls = l[r];  // per-lane partial sums -> the warp's l
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
             if (lane == 0) {
                 red_m[warp * ROWS + r] = m[r];
-                red_l[warp * ROWS + r] = l[r];
+                red_l[warp * ROWS + r] = ls;
             }
 #pragma unroll
             for (int e = 0; e < DPL; ++e) red_o[(warp * ROWS + r) * DV + lane * DPL + e] = acc[r][e];
@@ -339,8 +345,8 @@ cudaError_t launch_decode_t(const DecArgs &a, cudaStream_t st) {
 }  // namespace
 
 int decode_nsplit(int64_t bh_kv, int64_t n_kv) {
-    // one CTA per SM (the V ring is ~200 KB): about 4 waves over 148 SMs, each split >= 2 V blocks
-    int64_t want = (148 * 4 + bh_kv - 1) / bh_kv;
+    // one CTA per SM (the V ring is ~200 KB): about SFA_DEC_WAVES waves over 148 SMs, each split >= 2 V blocks
+    int64_t want = (148 * SFA_DEC_WAVES + bh_kv - 1) / bh_kv;
     const int64_t maxs = (n_kv + 2 * DB - 1) / (2 * DB);
     if (want > maxs) want = maxs;
     if (want < 1) want = 1;
