@@ -344,14 +344,28 @@ cudaError_t launch_decode_t(const DecArgs &a, cudaStream_t st) {
 
 }  // namespace
 
+// keys per split: a multiple of 32 (one consumer warp's slice); splits need not be whole V blocks
+int64_t decode_chunk(int64_t n_kv, int nsplit) { return ((n_kv + nsplit - 1) / nsplit + 31) / 32 * 32; }
+
 int decode_nsplit(int64_t bh_kv, int64_t n_kv) {
-    // one CTA per SM (the V ring is ~200 KB): about SFA_DEC_WAVES waves over 148 SMs, each split >= 2 V blocks
-    int64_t want = (148 * SFA_DEC_WAVES + bh_kv - 1) / bh_kv;
+    // one CTA per SM (the V ring is ~200 KB).  Pick the split count that minimises the streaming time
+    // waves x keys-per-CTA plus a per-wave ramp (first V block latency + merge, ~512 keys' worth),
+    // among splits of >= 2 V blocks and at most SFA_DEC_WAVES * 2 waves: a last wave that is mostly
+    // empty costs as much as a full one.
     const int64_t maxs = (n_kv + 2 * DB - 1) / (2 * DB);
-    if (want > maxs) want = maxs;
-    if (want < 1) want = 1;
-    if (want > 4096) want = 4096;
-    return (int)want;
+    int best = 1;
+    double best_cost = 1e300;
+    for (int64_t s = 1; s <= maxs && s <= 4096; ++s) {
+        const int64_t ctas = bh_kv * s;
+        const int64_t waves = (ctas + 147) / 148;
+        if (waves > 2 * SFA_DEC_WAVES && s > 1) break;
+        const double cost = (double)waves * ((double)decode_chunk(n_kv, (int)s) + 512.0);
+        if (cost < best_cost * 0.999) {
+            best_cost = cost;
+            best = (int)s;
+        }
+    }
+    return best;
 }
 
 size_t decode_workspace_bytes(int64_t bh_kv, int64_t n_kv, int d_v) {
@@ -383,7 +397,7 @@ cudaError_t launch_decode(const AttnParams &p, int d, int d_v, cudaStream_t st, 
     a.causal = p.causal;
     a.c_scale = p.scale_log2;
     a.nsplit = decode_nsplit((int64_t)p.B * p.H_kv, p.n_kv);
-    a.chunk = ((p.n_kv + a.nsplit - 1) / a.nsplit + DB - 1) / DB * DB;  // whole V blocks per split
+    a.chunk = decode_chunk(p.n_kv, a.nsplit);
     if (rows <= 4) return d_v == 64 ? launch_decode_t<64, 4>(a, st) : launch_decode_t<128, 4>(a, st);
     if (rows <= 8) return d_v == 64 ? launch_decode_t<64, 8>(a, st) : launch_decode_t<128, 8>(a, st);
     return d_v == 64 ? launch_decode_t<64, 16>(a, st) : launch_decode_t<128, 16>(a, st);
