@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--edges-only", action="store_true",
                     help="reading A1/R2 (SURVEY 8(f) N4): only pairs whose supports intersect enter the softmax")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dense-context", action="store_true", help="skip the dense SDPA context timing")
     ap.add_argument("--k", type=int, default=None, help="override the code size k (sweep)")
     ap.add_argument("--mode", default="forward", choices=["forward", "decode", "bwd"],
                     help="decode: SURVEY 8(f) N2, one new query row per sequence over a cached K/V of the config's n")
@@ -151,6 +152,16 @@ def oracle_sample(W, seed, n_rows, n_topk_rows, threads):
                       f"linear extrapolation to the full {B}x{H}x{n} workload"}
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def run_reference(args, W, rank):
     if rank != 0:
         return
@@ -174,7 +185,7 @@ def run_reference(args, W, rank):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded counter-based generator, DESIGN.md input recipe)",
             "config": config_of(args, W),
-            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "oracle", "cpu_model": cpu_model(),
                              "sample": r["sample"]},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -297,6 +308,31 @@ def run_decode(args, W, rank, world, local):
                      offset=rank * B * H_kv * n * d_v)
     qi, qv = sfa.topk_codes(Qn, k)
     ki, kv = sfa.topk_codes(K, k)  # the cache, coded once (not part of a decode step)
+    # context only: the same decode step over a DENSE bf16 K/V cache through torch SDPA (flash decode
+    # backend), L2 flushed the same way -- what the k-sparse cache replaces
+    dense_ctx = None
+    if rank == 0 and not args.no_dense_context:
+        try:
+            import torch.nn.functional as F
+            fl = torch.empty(L2_FLUSH_MB * 2 ** 20, dtype=torch.uint8, device=dev)
+            for _ in range(3):
+                F.scaled_dot_product_attention(Qn, K, V, enable_gqa=True)
+            tms = []
+            for _ in range(10):
+                fl.zero_()
+                c0 = torch.cuda.Event(enable_timing=True); c1 = torch.cuda.Event(enable_timing=True)
+                c0.record()
+                F.scaled_dot_product_attention(Qn, K, V, enable_gqa=True)
+                c1.record()
+                torch.cuda.synchronize()
+                tms.append(c0.elapsed_time(c1))
+            del fl
+            dms = sum(tms) / len(tms)
+            dense_ctx = {"dense_sdpa_ms": dms, "dense_cache_bytes": B * H_kv * n * (d + d_v) * 2,
+                         "dense_sdpa_gbs": B * H_kv * n * (d + d_v) * 2 / (dms / 1e3) / 1e9,
+                         "note": "torch SDPA (bf16, GQA) over the dense K/V cache of the same shape; context only"}
+        except Exception as ex:
+            dense_ctx = {"dense_sdpa_error": str(ex)[:200]}
     del K
     desc = sfa.make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k, d_v=d_v, n_q=1, n_kv=n, q_pos0=n - 1,
                          kernel=sfa.KERNEL_DECODE)
@@ -351,7 +387,8 @@ def run_decode(args, W, rank, world, local):
                              "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
                              "traffic": None, "algorithmic_bytes_per_step": cache_bytes + io_bytes,
                              "dense_kv_cache_bytes_for_comparison": B * H_kv * n * (d + d_v) * 2},
-                "cpu_baseline": None, "e2e": None, "gpu_launches": 2 * args.steps, "clocks": clk.summary()}
+                "cpu_baseline": None, "e2e": None, "gpu_launches": 2 * args.steps, "clocks": clk.summary(),
+                "context": dense_ctx}
         print(json.dumps(line), flush=True)
 
 
@@ -622,6 +659,31 @@ def main():
                       "D2H of neighbouring chunks overlap; synchronised)"}
         del qh, kh, vh, oh, lh, scratch, bufs
 
+    # context only (not a step, not a target): dense causal attention on the same shapes through torch's
+    # SDPA (FlashAttention/cuDNN backend on B200), bf16 Q, K, V with GQA -- what the codes replace
+    context = None
+    if rank == 0 and world == 1 and W.dtype == "bf16" and not args.no_dense_context:
+        try:
+            import torch.nn.functional as F
+            qd, kd, vd = Q, K, V
+            for _ in range(2):
+                F.scaled_dot_product_attention(qd, kd, vd, is_causal=W.causal, enable_gqa=True)
+            torch.cuda.synchronize()
+            c0 = torch.cuda.Event(enable_timing=True); c1 = torch.cuda.Event(enable_timing=True)
+            c0.record()
+            for _ in range(5):
+                F.scaled_dot_product_attention(qd, kd, vd, is_causal=W.causal, enable_gqa=True)
+            c1.record()
+            torch.cuda.synchronize()
+            dense_ms = c0.elapsed_time(c1) / 5
+            dpairs = B * H * accounting.causal_pairs(n, n, 0, W.causal)
+            context = {"dense_sdpa_ms": dense_ms, "dense_sdpa_tflops": 2.0 * (d + d_v) * dpairs / (dense_ms / 1e3) / 1e12,
+                       "sfa_attention_ms": stage_ms[3], "sfa_step_ms": ms_per_step,
+                       "note": "torch.nn.functional.scaled_dot_product_attention(bf16, causal, GQA) on the dense "
+                               "Q, K, V of the same step; context only, not part of the step or a target"}
+        except Exception as ex:  # context is optional
+            context = {"dense_sdpa_error": str(ex)[:200]}
+
     pk = peaks()
     attn_ms = stage_ms[3]
     pairs = B * H * accounting.causal_pairs(n, n, 0, W.causal)
@@ -664,6 +726,7 @@ def main():
         n_rows = int(max(1024, min(W.H * W.n // 2, 1024 * 16.0 / max(probe["t_sample"], 1e-3))))
         r = oracle_sample(W, seed, n_rows, 2048, threads)
         cpu = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": threads, "kind": "oracle",
+               "cpu_model": cpu_model(),
                "sample": r["sample"], "sample_seconds": r["t_sample"]}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -677,7 +740,7 @@ def main():
                 "pairs_per_s": pairs * world / (ms_per_step / 1e3),
                 "wall_s_timed_region": t_wall,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (5 + int(args.edges_only) if sm100 else 4) * args.steps,
-                "clocks": clk.summary()}
+                "clocks": clk.summary(), "context": context}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

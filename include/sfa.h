@@ -117,7 +117,9 @@ typedef struct {
 SFA_API size_t sfa_attn_workspace_bytes(const sfa_attn_desc *desc);
 
 /* O, LSE = FlashSFA forward.
- *   q_idx [B][H][n_q][k] u8,  q_val [B][H][n_q][k]   (stage-1 codes of Q)
+ *   q_idx [B][H][n_q][k] u8,  q_val [B][H][n_q][k]   (stage-1 codes of Q: every row's indices distinct and
+ *                                                      ascending, as sfa_topk_codes writes them (A4); with
+ *                                                      k = d the kernels rely on idx[t] = t)
  *   k_idx [B][H_kv][n_kv][k] u8, k_val [B][H_kv][n_kv][k]
  *   v     [B][H_kv][n_kv][d_v]       o [B][H][n_q][d_v] (dtype)       lse [B][H][n_q] fp32, natural log
  *   workspace: >= sfa_attn_workspace_bytes(desc) device bytes (else SFA_ERR_RESOURCE), 16-aligned.

@@ -157,15 +157,37 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
         for (int j = 0; j < nt; ++j) {
             const uint32_t sbuf = dq_sbuf(j);
             mbar_wait(BAR(S_FULL + (j & 1)), (j >> 1) & 1);
-            mbar_wait(BAR(DP_FULL), j & 1);
             tc_fence_after();
             int64_t l64 = kend - (int64_t)j * BN;
             const int lim = l64 < 0 ? 0 : (l64 > BN ? BN : (int)l64);
-#pragma unroll 1
-            for (int c = 0; c < 2; ++c) {  // 32 keys at a time; dS overwrites S columns this group has read
+            // P-phase (needs S only: runs while dP(j) is still on the tensor pipe); p kept in fp32
+            float pp[2][32];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
                 const int cc = 2 * grp + c;
-                uint32_t s[32], dp[32], pk[16];
+                uint32_t s[32];
                 tmem_ld32(tmem + lo + sbuf + 32 * cc, s);
+                tmem_ld_wait();
+                auto chunk = [&](auto masked) {  // masks only where the diagonal / ragged end cuts the chunk
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) {
+                        float p = fast_exp2(fmaf(__uint_as_float(s[e]), cs, -lse2));
+                        if (decltype(masked)::value && 32 * cc + e >= lim) p = 0.f;
+                        pp[c][e] = p;
+                    }
+                };
+                if (lim >= 32 * cc + 32)
+                    chunk(std::false_type{});
+                else
+                    chunk(std::true_type{});
+            }
+            // dS-phase: dS = P (.) (dP - D), bf16 over the S columns this group has read
+            mbar_wait(BAR(DP_FULL), j & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int cc = 2 * grp + c;
+                uint32_t dp[32], pk[16];
                 tmem_ld32(tmem + lo + 128 + 32 * cc, dp);
                 tmem_ld_wait();
                 if (c == 1) {  // this warp is done with dP(j): dP(j+1) may be issued
@@ -173,24 +195,10 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
                     __syncwarp();
                     if (lane == 0) mbar_arrive(BAR(DP_FREE));
                 }
-                auto chunk = [&](auto masked) {  // masks only where the diagonal / ragged end cuts the chunk
 #pragma unroll
-                    for (int e = 0; e < 16; ++e) {
-                        const int k0 = 32 * cc + 2 * e;
-                        float p0 = fast_exp2(fmaf(__uint_as_float(s[2 * e]), cs, -lse2));
-                        float p1 = fast_exp2(fmaf(__uint_as_float(s[2 * e + 1]), cs, -lse2));
-                        if (decltype(masked)::value) {
-                            if (k0 >= lim) p0 = 0.f;
-                            if (k0 + 1 >= lim) p1 = 0.f;
-                        }
-                        pk[e] = pack_bf16x2(p0 * (__uint_as_float(dp[2 * e]) - Di),
-                                            p1 * (__uint_as_float(dp[2 * e + 1]) - Di));
-                    }
-                };
-                if (lim >= 32 * cc + 32)
-                    chunk(std::false_type{});
-                else
-                    chunk(std::true_type{});
+                for (int e = 0; e < 16; ++e)
+                    pk[e] = pack_bf16x2(pp[c][2 * e] * (__uint_as_float(dp[2 * e]) - Di),
+                                        pp[c][2 * e + 1] * (__uint_as_float(dp[2 * e + 1]) - Di));
                 tmem_st16(tmem + lo + sbuf + 64 * grp + 16 * c, pk);
             }
             tmem_st_wait();

@@ -29,6 +29,22 @@ __device__ __forceinline__ void prefetch_code_row(const uint8_t *idx, const uint
 template <int D>
 __device__ __forceinline__ void densify_row(uint32_t tile, int rows, int r, bool valid, const uint8_t *__restrict__ idx,
                                             const uint16_t *__restrict__ val, int k) {
+    if (k == D && valid) {
+        // k = d: every feature is selected and the indices are ascending (A4), so idx[t] = t and the
+        // row IS the value vector -- 16-byte copies into the swizzled row, no zeroing, no scatter
+        const uint4 *src = reinterpret_cast<const uint4 *>(val);
+#pragma unroll
+        for (int kb = 0; kb < D / 64; ++kb)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const uint4 w = __ldg(src + kb * 8 + c);
+                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(tile + kb * rows * 128 + r * 128 +
+                                                                                ((c ^ (r & 7)) << 4)),
+                             "r"(w.x), "r"(w.y), "r"(w.z), "r"(w.w)
+                             : "memory");
+            }
+        return;
+    }
 #pragma unroll
     for (int kb = 0; kb < D / 64; ++kb)
 #pragma unroll

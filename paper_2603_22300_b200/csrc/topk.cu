@@ -249,9 +249,40 @@ __global__ void __launch_bounds__(TK_ROWS) topk_rows_bf16_kernel(const uint16_t 
 }
 
 // host launcher (called from api.cu after validation)
+// k = d: Topk_k is the identity (every entry selected, indices ascending): idx[r][t] = t, val = x bit
+// copy, non-finite entries still flagged (A14).  One thread per element, HBM-bound.
+template <typename T>
+__global__ void __launch_bounds__(256) topk_identity_kernel(const T *__restrict__ x, int64_t rows, int d, int64_t ld,
+                                                            uint8_t *__restrict__ idx, T *__restrict__ val,
+                                                            uint32_t *status_word) {
+    const int64_t n = rows * d;
+    bool bad = false;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / d;
+        const int c = (int)(e % d);
+        const T v = x[r * ld + c];
+        val[e] = v;
+        idx[e] = (uint8_t)c;
+        const uint32_t mag = sizeof(T) == 2 ? ((uint32_t)v & 0x7FFFu) : ((uint32_t)v & 0x7FFFFFFFu);
+        bad |= sizeof(T) == 2 ? (mag >= 0x7F80u) : (mag >= 0x7F800000u);
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0 && status_word != nullptr) atomicOr(status_word, 1u);
+}
+
 cudaError_t launch_topk(const void *x, bool bf16, int64_t rows, int d, int64_t ld, int k, uint8_t *idx, void *val,
                         uint32_t *status_word, cudaStream_t stream) {
     if (rows == 0) return cudaSuccess;
+    if (k == d) {
+        const int64_t n = rows * d;
+        const unsigned g = (unsigned)((n + 255) / 256 < 148 * 32 ? (n + 255) / 256 : 148 * 32);
+        if (bf16)
+            topk_identity_kernel<uint16_t><<<g, 256, 0, stream>>>((const uint16_t *)x, rows, d, ld, idx, (uint16_t *)val,
+                                                                  status_word);
+        else
+            topk_identity_kernel<uint32_t><<<g, 256, 0, stream>>>((const uint32_t *)x, rows, d, ld, idx, (uint32_t *)val,
+                                                                  status_word);
+        return cudaGetLastError();
+    }
     int sms = 148;
     int dev = 0;
     cudaGetDevice(&dev);

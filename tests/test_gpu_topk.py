@@ -66,10 +66,11 @@ def test_nonfinite_flag(lib, dtype):
     x[30, 2] = np.nan
     if dtype == "bf16":
         x = inputs.f32_to_bf16_bits(x)
-    _, _, st = run(lib, x, dtype, 8)
-    assert st & 1
-    x2 = inputs.gen(5, 1, (40, 64), dtype)
-    assert run(lib, x2, dtype, 8)[2] == 0
+    for k in (8, 64):  # k = d takes the identity kernel: it must flag too
+        _, _, st = run(lib, x, dtype, k)
+        assert st & 1
+        x2 = inputs.gen(5, 1, (40, 64), dtype)
+        assert run(lib, x2, dtype, k)[2] == 0
 
 
 def test_qwen3_shape_all_rows(lib):
