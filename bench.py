@@ -44,6 +44,8 @@ def parse():
                     help="reading A1/R2 (SURVEY 8(f) N4): only pairs whose supports intersect enter the softmax")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dense-context", action="store_true", help="skip the dense SDPA context timing")
+    ap.add_argument("--fused-q", action="store_true",
+                    help="step 1 on Q inside the attention prologue (sfa_attn_fwd_fused_q, N3(ii) ablation)")
     ap.add_argument("--k", type=int, default=None, help="override the code size k (sweep)")
     ap.add_argument("--mode", default="forward", choices=["forward", "decode", "bwd"],
                     help="decode: SURVEY 8(f) N2, one new query row per sequence over a cached K/V of the config's n")
@@ -198,6 +200,9 @@ def config_of(args, W):
             f"({args.gpus} GPU{'s' if args.gpus > 1 else ''}), no data-path collective",
             "kernel": args.kernel,
             "semantics": "R2 edges-only (A1/R2)" if getattr(args, "edges_only", False) else "R1 (A1)",
+            "q_topk": "fused into the attention prologue (N3(ii)); stage_ms.attn includes it"
+                      if (getattr(args, "fused_q", False) and not getattr(args, "edges_only", False) and W.d_v == 128
+                          and W.dtype == "bf16" and args.kernel in ("auto", "ot")) else "own kernel",
             "l2": f"explicit {L2_FLUSH_MB} MB write between timed steps (outside the step events); "
                   "inputs+outputs also exceed the 126 MB L2"}
 
@@ -577,17 +582,24 @@ def main():
     P = lambda t: ctypes.c_void_p(t.data_ptr())
     dcode = desc.dtype
 
+    fused_q = (W.dtype == "bf16" and d_v == 128 and args.kernel in ("auto", "ot") and not args.edges_only
+               and args.fused_q)
+
     def step(ev=None):
         # stage 1 on Q, stage 1 on K, step 3 (V prep for sm100 / buckets for simt), steps 4-8 attention
         if ev: ev[0].record()
-        r1 = L.sfa_topk_codes(P(Q), dcode, B * H * n, d, d, k, P(q_idx), P(q_val), P(status), st())
+        r1 = 0 if fused_q else L.sfa_topk_codes(P(Q), dcode, B * H * n, d, d, k, P(q_idx), P(q_val), P(status), st())
         if ev: ev[1].record()
         r2 = L.sfa_topk_codes(P(K), dcode, B * H_kv * n, d, d, k, P(k_idx), P(k_val), P(status), st())
         if ev: ev[2].record()
         r3 = L.sfa_attn_prepare(ctypes.byref(desc), P(k_idx), P(k_val), P(V), P(ws), ws.numel(), st())
         if ev: ev[3].record()
-        r4 = L.sfa_attn_fwd_prepared(ctypes.byref(desc), P(q_idx), P(q_val), P(k_idx), P(k_val), P(V), P(O), P(LSE),
-                                     P(ws), ws.numel(), st())
+        if fused_q:  # step 1 on Q inside the attention prologue (N3(ii)); the q codes are still written out
+            r4 = L.sfa_attn_fwd_fused_q(ctypes.byref(desc), P(Q), P(k_idx), P(k_val), P(V), P(O), P(LSE), P(q_idx),
+                                        P(q_val), P(status), P(ws), ws.numel(), st())
+        else:
+            r4 = L.sfa_attn_fwd_prepared(ctypes.byref(desc), P(q_idx), P(q_val), P(k_idx), P(k_val), P(V), P(O),
+                                         P(LSE), P(ws), ws.numel(), st())
         if ev: ev[4].record()
         if r1 or r2 or r3 or r4:
             raise RuntimeError(f"sfa call failed: {(r1, r2, r3, r4)}")
@@ -693,16 +705,18 @@ def main():
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         try:
-            ent = json.load(open(tp)).get(args.config, {}).get(f"attn_{args.kernel}")
+            ent = json.load(open(tp)).get(args.config, {}).get(f"attn_{args.kernel}" + ("_fusedq" if fused_q else ""))
             traffic = ent["dram_bytes_per_launch"] if ent else None
         except Exception:
             traffic = None
     topk_bytes = W.topk_bytes()
+    if fused_q:  # only the K rows go through the stand-alone top-k kernel
+        topk_bytes = B * H_kv * n * (d * 2 + k * 3)
     sm100 = W.dtype == "bf16" and args.kernel != "simt"
     kname = {"auto": "attn_sm100_ot_kernel" if d_v == 128 else "attn_sm100_kernel", "sm100": "attn_sm100_kernel",
              "ot": "attn_sm100_ot_kernel", "pair": "attn_sm100_pair_kernel", "wide": "attn_sm100_wide_kernel",
              "simt": "attn_simt_kernel"}[args.kernel if sm100 else "simt"]
-    roofline = {"bound": "alu", "kernel": kname + " (steps 4-8)",
+    roofline = {"bound": "alu", "kernel": kname + (" (step 1 on Q fused + steps 4-8)" if fused_q else " (steps 4-8)"),
                 "achieved": achieved / 1e9, "peak": mufu_peak / 1e9,
                 "unit": "G pairs/s (1 MUFU ex2 per allowed causal pair)",
                 "frac": achieved / mufu_peak, "traffic": traffic,
@@ -739,7 +753,7 @@ def main():
                 "interactions_per_s": W.expected_interactions / (ms_per_step / 1e3) * world,
                 "pairs_per_s": pairs * world / (ms_per_step / 1e3),
                 "wall_s_timed_region": t_wall,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (5 + int(args.edges_only) if sm100 else 4) * args.steps,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (5 + int(args.edges_only) - int(fused_q) if sm100 else 4) * args.steps,
                 "clocks": clk.summary(), "context": context}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -143,6 +143,19 @@ SFA_API sfa_status sfa_attn_fwd_prepared(const sfa_attn_desc *desc, const uint8_
                                          const uint8_t *k_idx, const void *k_val, const void *v, void *o, float *lse,
                                          const void *workspace, size_t workspace_bytes, sfa_stream_t stream);
 
+/* Steps 1 (on Q) to 8 in one kernel: the attention prologue selects the top-k of
+ * every DENSE query row itself (the same selection code as sfa_topk_codes, so the support and the result
+ * are bit-identical to sfa_topk_codes + sfa_attn_fwd_prepared), builds Q~ on chip and, if q_idx_out /
+ * q_val_out are non-null (both or neither), also writes the codes [B][H][n_q][k] it selected.
+ *   q: dense bf16 [B][H][n_q][d], 16-byte aligned.  k codes, v, workspace as sfa_attn_fwd_prepared
+ *   (workspace prepared by sfa_attn_prepare).  status_word (nullable): bit 0 OR-ed on non-finite q (A14).
+ *   Supported when the desc resolves to SFA_KERNEL_SM100_OT (bf16, d_v = 128) with edges_only = 0;
+ *   otherwise SFA_ERR_UNSUPPORTED.  Measured slower than the two-kernel path at Qwen3-32K (the per-CTA
+ *   top-k prologue sits on every CTA's critical path), so sfa_forward does not use it. */
+SFA_API sfa_status sfa_attn_fwd_fused_q(const sfa_attn_desc *desc, const void *q, const uint8_t *k_idx,
+                                        const void *k_val, const void *v, void *o, float *lse, uint8_t *q_idx_out,
+                                        void *q_val_out, uint32_t *status_word, const void *workspace,
+                                        size_t workspace_bytes, sfa_stream_t stream);
 /* ------------------------------------------------------------------------------------------
  * Backward: the straight-through rule of P:L103-112 (Sec. 3.1 "Backward
  * computation", Eq. topk_grad) composed with the softmax-attention backward.

@@ -162,6 +162,11 @@ sfa_status run_attn(const sfa_attn_desc *d, const uint8_t *q_idx, const void *q_
 
 bool codes_aligned(const void *a, const void *b) { return aligned16(a) && aligned16(b); }
 
+// the fused step-1-on-Q path (N3(ii)) exists for the SM100_OT kernel with R1 semantics
+bool fusable(const sfa_attn_desc *d) {
+    return d->dtype == SFA_BF16 && !d->edges_only && resolve_kernel(d) == SFA_KERNEL_SM100_OT;
+}
+
 }  // namespace
 
 extern "C" {
@@ -265,6 +270,27 @@ sfa_status sfa_attn_fwd_prepared(const sfa_attn_desc *desc, const uint8_t *q_idx
     return run_attn_prepared(desc, q_idx, q_val, k_idx, k_val, v, o, lse, (void *)workspace, (cudaStream_t)stream);
 }
 
+sfa_status sfa_attn_fwd_fused_q(const sfa_attn_desc *desc, const void *q, const uint8_t *k_idx, const void *k_val,
+                                const void *v, void *o, float *lse, uint8_t *q_idx_out, void *q_val_out,
+                                uint32_t *status_word, const void *workspace, size_t workspace_bytes,
+                                sfa_stream_t stream) {
+    sfa_status s = validate_desc(desc);
+    if (s != SFA_OK) return s;
+    if (!fusable(desc)) return SFA_ERR_UNSUPPORTED;
+    if (!q || !k_idx || !k_val || !v || !o || !lse || !workspace) return SFA_ERR_INVALID_ARGUMENT;
+    if ((q_idx_out == nullptr) != (q_val_out == nullptr)) return SFA_ERR_INVALID_ARGUMENT;
+    if (!aligned16(q) || !codes_aligned(k_idx, k_val) || !aligned16(v) || !aligned16(o) || ((uintptr_t)lse & 3u) ||
+        (q_idx_out && !codes_aligned(q_idx_out, q_val_out)) || ((uintptr_t)status_word & 3u))
+        return SFA_ERR_INVALID_ARGUMENT;
+    if (workspace_bytes < ws_bytes(desc)) return SFA_ERR_RESOURCE;
+    AttnParams p = make_params(desc, nullptr, nullptr, k_idx, k_val, v, o, lse, workspace);
+    p.q_dense = q;
+    p.q_idx_out = q_idx_out;
+    p.q_val_out = q_val_out;
+    p.status_word = status_word;
+    return from_launch(launch_attn_sm100_ot(p, desc->d, desc->d_v, (cudaStream_t)stream, nullptr));
+}
+
 size_t sfa_attn_bwd_workspace_bytes(const sfa_attn_desc *desc) {
     if (validate_desc(desc) != SFA_OK) return 0;
     return (size_t)desc->B * desc->H * desc->n_q * sizeof(float);
@@ -315,13 +341,27 @@ static sfa_status forward_impl(const sfa_attn_desc *desc, const void *q, const v
                                float *lse, uint8_t *S, uint32_t *status, cudaStream_t st) {
     const Scratch L = scratch_layout(desc);
     const bool bf16 = desc->dtype == SFA_BF16;
-    cudaError_t e = launch_topk(q, bf16, (int64_t)desc->B * desc->H * desc->n_q, desc->d, desc->d, desc->k,
-                                S + L.q_idx, S + L.q_val, status, st);
-    if (e != cudaSuccess) return SFA_ERR_CUDA;
+    cudaError_t e;
+    // step 1 on Q as its own kernel: measured faster than the fused prologue (N3(ii))
+    const bool fuse = false;
+    if (!fuse) {
+        e = launch_topk(q, bf16, (int64_t)desc->B * desc->H * desc->n_q, desc->d, desc->d, desc->k, S + L.q_idx,
+                        S + L.q_val, status, st);
+        if (e != cudaSuccess) return SFA_ERR_CUDA;
+    }
     e = launch_topk(k, bf16, (int64_t)desc->B * desc->H_kv * desc->n_kv, desc->d, desc->d, desc->k, S + L.k_idx,
                     S + L.k_val, status, st);
     if (e != cudaSuccess) return SFA_ERR_CUDA;
-    return run_attn(desc, S + L.q_idx, S + L.q_val, S + L.k_idx, S + L.k_val, v, o, lse, S + L.ws, st);
+    if (!fuse || !fusable(desc))
+        return run_attn(desc, S + L.q_idx, S + L.q_val, S + L.k_idx, S + L.k_val, v, o, lse, S + L.ws, st);
+    sfa_status s = run_prepare(desc, S + L.k_idx, S + L.k_val, v, S + L.ws, st);
+    if (s != SFA_OK) return s;
+    AttnParams p = make_params(desc, nullptr, nullptr, S + L.k_idx, S + L.k_val, v, o, lse, S + L.ws);
+    p.q_dense = q;
+    p.q_idx_out = S + L.q_idx;  // the codes of Q stay available (e.g. for the backward)
+    p.q_val_out = S + L.q_val;
+    p.status_word = status;
+    return from_launch(launch_attn_sm100_ot(p, desc->d, desc->d_v, st, nullptr));
 }
 
 sfa_status sfa_forward(const sfa_attn_desc *desc, const void *q, const void *k, const void *v, void *o, float *lse,

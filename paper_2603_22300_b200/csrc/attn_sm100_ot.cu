@@ -31,6 +31,7 @@
 #include <mutex>
 
 #include "densify.cuh"
+#include "topk_row.cuh"
 #include "launch.cuh"
 #include "sm100.cuh"
 
@@ -140,7 +141,11 @@ __device__ __forceinline__ void prefetch_l1(const void *ptr) {
 // tile each softmax thread ORs the tile's feature bitsets kf[f] over the k features of its row:
 // eh[q] bit c = "key 32q+c shares a feature with this row" (k 16-byte loads, issued before the
 // wait for S), ANDs in the causal / ragged bound, and excludes the other keys like the causal mask.
-template <int D, bool DBG, bool EDGE>
+// FUSEQ: step 1 on Q fused into the prologue -- the softmax thread of query row r
+// of tile t loads the DENSE bf16 Q row, selects its top-k with the same code as the stand-alone kernel
+// (topk_row.cuh), writes the masked row straight into the swizzled Q~ tile and (optionally) the row's
+// code to q_idx_out / q_val_out; the decompression warps then only build K~.
+template <int D, bool DBG, bool EDGE, bool FUSEQ>
 __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid_constant__ CUtensorMap tmap_v,
                                                                       const OtArgs a) {
     using C = Cfg<D>;
@@ -172,6 +177,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         for (int i = 0; i < NBAR; ++i) {
             uint32_t cnt = 1;
             if (i == KFULL || i == KFULL + 1 || i == SEMPTY || i == SEMPTY + 1 || i == QFULL) cnt = 4;
+            if (FUSEQ && i == QFULL) cnt = 8;  // the eight softmax warps build Q~
             if (i == PFULL || i == PFULL + 1) cnt = 8;
             mbar_init(BAR(i), cnt);
         }
@@ -198,6 +204,86 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         int64_t kend = p.n_kv;
         if (p.causal && p.q_pos0 + i + 1 < kend) kend = p.q_pos0 + i + 1;
         const float cs = a.c_scale;
+        if (FUSEQ) {
+            // ---- step 1 on this row: dense Q row -> top-k masks -> masked row into the Q~ tile
+            constexpr int NW = D / 2, NC = D / 8;  // words / 16-byte chunks per row
+            const int64_t qrow = ((int64_t)b * p.H + tl[t].h) * p.n_q + (row_ok ? i : 0);
+            {   // coalesced loads of the CTA's 256 dense rows into the (still unused) P buffer, 16-byte
+                // chunks XOR-swizzled by row so each thread then reads its own row conflict-free
+                const int tid = threadIdx.x;  // 0..255 = the eight softmax warps
+                uint8_t *stage = gbase + C::OFF_P;
+                for (int v = tid; v < 2 * BM * NC; v += 2 * BM) {
+                    const int rr = v / NC, c = v % NC, tt = rr / BM, ri = rr % BM;
+                    const int64_t ii = (int64_t)tl[tt].qb * BM + ri;
+                    uint4 w = make_uint4(0u, 0u, 0u, 0u);
+                    if (tl[tt].valid && ii < p.n_q)
+                        w = __ldcs(reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(p.q_dense) +
+                                                                   (((int64_t)b * p.H + tl[tt].h) * p.n_q + ii) * D) + c);
+                    *reinterpret_cast<uint4 *>(stage + rr * D * 2 + ((c ^ (rr & 15) & (NC - 1)) << 4)) = w;
+                }
+                named_bar_sync(3, 2 * BM);
+            }
+            uint32_t raw[NW], ab[NW];
+            {
+                const int rr = t * BM + r;
+                const uint8_t *stage = gbase + C::OFF_P + rr * D * 2;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const uint4 w = *reinterpret_cast<const uint4 *>(stage + ((c ^ (rr & 15) & (NC - 1)) << 4));
+                    raw[4 * c] = w.x; raw[4 * c + 1] = w.y; raw[4 * c + 2] = w.z; raw[4 * c + 3] = w.w;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < NW; ++q) ab[q] = raw[q] & 0x7FFF7FFFu;
+            if (row_ok && p.status_word != nullptr && tk::row_max_key(ab) >= 0x7F80u) atomicOr(p.status_word, 1u);
+            uint32_t gm[D / 32];
+            tk::select_masks(ab, p.k, gm);
+            if (!row_ok) {
+#pragma unroll
+                for (int w = 0; w < D / 32; ++w) gm[w] = 0u;
+            }
+            const uint32_t qt = sbase + C::OFF_Q + t * C::QT;
+#pragma unroll
+            for (int kb = 0; kb < D / 64; ++kb)
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    uint32_t o4[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int W = 4 * (8 * kb + c) + q;  // word = features 2W, 2W + 1
+                        const uint32_t b2 = (gm[W >> 4] >> (2 * (W & 15))) & 3u;
+                        o4[q] = raw[W] & (((b2 & 1u) * 0xFFFFu) | ((b2 >> 1) * 0xFFFF0000u));
+                    }
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(qt + kb * BM * 128 + r * 128 +
+                                                                                    ((c ^ (r & 7)) << 4)),
+                                 "r"(o4[0]), "r"(o4[1]), "r"(o4[2]), "r"(o4[3])
+                                 : "memory");
+                }
+            if (row_ok && p.q_idx_out != nullptr) {  // the row's code, ascending (A4)
+                uint8_t *oi = p.q_idx_out + qrow * p.k;
+                uint16_t *ov = static_cast<uint16_t *>(p.q_val_out) + qrow * p.k;
+                int pos = 0;
+#pragma unroll
+                for (int w = 0; w < D / 32; ++w) {
+                    uint32_t mm = gm[w];
+                    while (mm != 0u) {
+                        const int f = 32 * w + (__ffs(mm) - 1);
+                        mm &= mm - 1u;
+                        oi[pos] = (uint8_t)f;
+                        uint16_t vbits;  // re-read from the Q~ row just written (no dynamic register index)
+                        asm volatile("ld.shared.u16 %0, [%1];"
+                                     : "=h"(vbits)
+                                     : "r"(qt + (f >> 6) * BM * 128 + r * 128 + ((((f >> 3) & 7) ^ (r & 7)) << 4) +
+                                           (f & 7) * 2));
+                        ov[pos] = vbits;
+                        ++pos;
+                    }
+                }
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(BAR(QFULL));
+        }
         float *f_t = fac + t * BM;
         const uint32_t prow = sbase + C::OFF_P + (uint32_t)(t * BM + r) * 128u;  // row t*128+r, key atom 0
         const int bar_id = 1 + t;
@@ -410,16 +496,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         const int k = p.k;
         const uint16_t *qv = reinterpret_cast<const uint16_t *>(p.q_val);
         const uint16_t *kv = reinterpret_cast<const uint16_t *>(p.k_val);
+        if (!FUSEQ) {
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-            const int64_t i = (int64_t)tl[t].qb * BM + r;
-            const bool ok = tl[t].valid && i < p.n_q;
-            const int64_t row = ((int64_t)b * p.H + tl[t].h) * p.n_q + i;
-            densify_row<D>(sbase + C::OFF_Q + t * C::QT, BM, r, ok, p.q_idx + row * k, qv + row * k, k);
+            for (int t = 0; t < 2; ++t) {
+                const int64_t i = (int64_t)tl[t].qb * BM + r;
+                const bool ok = tl[t].valid && i < p.n_q;
+                const int64_t row = ((int64_t)b * p.H + tl[t].h) * p.n_q + i;
+                densify_row<D>(sbase + C::OFF_Q + t * C::QT, BM, r, ok, p.q_idx + row * k, qv + row * k, k);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(BAR(QFULL));
         }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(BAR(QFULL));
         const int64_t kv0 = ((int64_t)b * p.H_kv + g) * p.n_kv;
         for (int j = 0; j < nt; ++j) {
             const int s = j % C::NK, u = j / C::NK;
@@ -549,8 +637,11 @@ cudaError_t launch_t(const OtArgs &a, cudaStream_t stream, int items) {
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    auto kern = p.edges_only ? (a.dbg != nullptr ? attn_sm100_ot_kernel<D, true, true> : attn_sm100_ot_kernel<D, false, true>)
-                             : (a.dbg != nullptr ? attn_sm100_ot_kernel<D, true, false> : attn_sm100_ot_kernel<D, false, false>);
+    auto kern = p.q_dense != nullptr ? attn_sm100_ot_kernel<D, false, false, true>
+                : p.edges_only ? (a.dbg != nullptr ? attn_sm100_ot_kernel<D, true, true, false>
+                                                   : attn_sm100_ot_kernel<D, false, true, false>)
+                               : (a.dbg != nullptr ? attn_sm100_ot_kernel<D, true, false, false>
+                                                   : attn_sm100_ot_kernel<D, false, false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     kern<<<items, NTHREADS, C::SMEM, stream>>>(tm, a);
@@ -562,6 +653,7 @@ cudaError_t launch_t(const OtArgs &a, cudaStream_t stream, int items) {
 cudaError_t launch_attn_sm100_ot(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg) {
     if ((d != 64 && d != 128) || d_v != DV) return cudaErrorNotSupported;
     if (p.edges_only && p.kfmask == nullptr) return cudaErrorInvalidValue;
+    if (p.q_dense != nullptr && (p.edges_only || dbg != nullptr)) return cudaErrorNotSupported;
     OtArgs a;
     a.p = p;
     a.nqb = (int)((p.n_q + BM - 1) / BM);

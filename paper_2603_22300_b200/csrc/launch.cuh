@@ -22,6 +22,12 @@ struct AttnParams {
     BucketLayout L;
     int32_t edges_only;      // reading A1/R2: only pairs whose supports intersect enter the softmax
     const uint32_t *kfmask;  // R2, SM100_OT: per key tile, per feature, the 128-bit set of keys selecting it
+    // fused step 1 on Q (SM100_OT, N3(ii)): dense bf16 Q [B][H][n_q][d] instead of q codes; the kernel
+    // optionally writes the codes it selected (q_idx_out / q_val_out) and flags non-finite Q
+    const void *q_dense = nullptr;
+    uint8_t *q_idx_out = nullptr;
+    void *q_val_out = nullptr;
+    uint32_t *status_word = nullptr;
 };
 
 // R2 feature bitsets of the key tiles (edges.cu): [B*H_kv][ceil(n_kv/128)][d][4] u32

@@ -8,6 +8,7 @@
 // taken lowest index first (A2) using a ballot-sliced exclusive prefix over lanes.  Output
 // is in ascending feature order (A4), values are bit copies (A7).  HBM-bound.
 #include "launch.cuh"
+#include "topk_row.cuh"
 
 namespace sfa {
 
@@ -148,71 +149,19 @@ __global__ void __launch_bounds__(TK_ROWS) topk_rows_bf16_kernel(const uint16_t 
 
     const bool active = t < nrows;
     uint32_t ab[NW];  // |x| bit patterns, two keys per word
-    uint32_t mx2 = 0;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
         const uint4 w = *reinterpret_cast<const uint4 *>(rowbuf + t * D * 2 + ((c ^ (t & 15) & (NC - 1)) << 4));
-        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            ab[4 * c + e] = ww[e] & 0x7FFF7FFFu;
-            uint32_t m;
-            asm("max.u16x2 %0, %1, %2;" : "=r"(m) : "r"(mx2), "r"(ab[4 * c + e]));
-            mx2 = m;
-        }
+        ab[4 * c + 0] = w.x & 0x7FFF7FFFu;
+        ab[4 * c + 1] = w.y & 0x7FFF7FFFu;
+        ab[4 * c + 2] = w.z & 0x7FFF7FFFu;
+        ab[4 * c + 3] = w.w & 0x7FFF7FFFu;
     }
-    const uint32_t mx = max(mx2 & 0xFFFFu, mx2 >> 16);
-    if (active && mx >= 0x7F80u && status_word != nullptr) atomicOr(status_word, 1u);
-
-    // #{key >= T} over the row, on the FP16 pipe: for finite non-negative bf16 the numeric order is the
-    // order of the bit patterns (subnormals kept: no .ftz), so set.ge.bf16x2 gives 1.0 per key >= T and
-    // four bf16x2 accumulators count exactly (<= 32 per half).  Non-finite rows are flagged above.
-    auto count_ge = [&](uint32_t T) {
-        const uint32_t t2 = T * 0x10001u;
-        uint32_t acc[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-        for (int i = 0; i < NW; ++i) {
-            uint32_t m;
-            asm("set.ge.bf16x2.bf16x2 %0, %1, %2;" : "=r"(m) : "r"(ab[i]), "r"(t2));
-            asm("add.rn.bf16x2 %0, %0, %1;" : "+r"(acc[i & 3]) : "r"(m));
-        }
-        uint32_t s01, s23, s;
-        asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(s01) : "r"(acc[0]), "r"(acc[1]));
-        asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(s23) : "r"(acc[2]), "r"(acc[3]));
-        asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(s) : "r"(s01), "r"(s23));  // <= 64 per half: exact
-        return (int)(__uint_as_float(s << 16) + __uint_as_float(s & 0xFFFF0000u));
-    };
-    // 3. largest T with #{key >= T} >= k
-    uint32_t T = 0;
-#pragma unroll 1
-    for (int bit = 14; bit >= 0; --bit) {
-        const uint32_t cand = T | (1u << bit);
-        if (count_ge(cand) >= k) T = cand;
-    }
-    // 4. selection bit masks (bit f = key f): key > T always, key == T for the lowest-index ties
+    if (active && tk::row_max_key(ab) >= 0x7F80u && status_word != nullptr) atomicOr(status_word, 1u);
+    // 3-4. threshold search and selection masks (topk_row.cuh)
     constexpr int NM = D / 32;
-    uint32_t gm[NM], em[NM];
-#pragma unroll
-    for (int w = 0; w < NM; ++w) gm[w] = em[w] = 0u;
-    const uint32_t tg = (T + 1u) * 0x10001u, te = T * 0x10001u;  // T + 1 <= 0x7F80 (+inf) on finite rows
-#pragma unroll
-    for (int i = 0; i < NW; ++i) {
-        uint32_t g, e;  // bf16 1.0 (0x3F80, bit 7 set) per true half
-        asm("set.ge.bf16x2.bf16x2 %0, %1, %2;" : "=r"(g) : "r"(ab[i]), "r"(tg));
-        asm("set.eq.bf16x2.bf16x2 %0, %1, %2;" : "=r"(e) : "r"(ab[i]), "r"(te));
-        gm[i >> 4] |= (((g >> 7) & 1u) | ((g >> 22) & 2u)) << (2 * (i & 15));
-        em[i >> 4] |= (((e >> 7) & 1u) | ((e >> 22) & 2u)) << (2 * (i & 15));
-    }
-    int need = k;
-#pragma unroll
-    for (int w = 0; w < NM; ++w) need -= __popc(gm[w]);
-#pragma unroll
-    for (int w = 0; w < NM; ++w)
-        while (need > 0 && em[w] != 0u) {  // lowest-index ties first (A2)
-            gm[w] |= em[w] & (0u - em[w]);
-            em[w] &= em[w] - 1u;
-            --need;
-        }
+    uint32_t gm[NM];
+    tk::select_masks(ab, k, gm);
     // 5. ascending compaction into the staging area (values re-read from the row in shared memory)
     uint8_t *my_i = oidx + t * k;
     uint16_t *my_v = oval + t * k;

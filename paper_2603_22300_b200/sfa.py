@@ -73,6 +73,7 @@ def lib() -> ctypes.CDLL:
             "sfa_gen_fill": ([P, I32, I64, I64, ctypes.c_uint64, I32, I32, I64, I32, I32, P], I32),
             "sfa_attn_bwd_workspace_bytes": ([D], SZ),
             "sfa_attn_bwd": ([D, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P], I32),
+            "sfa_attn_fwd_fused_q": ([D, P, P, P, P, P, P, P, P, P, P, SZ, P], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -86,7 +87,7 @@ EXPORTS = ("sfa_status_string", "sfa_topk_codes", "sfa_attn_workspace_bytes", "s
            "sfa_forward_host", "sfa_device_supported", "sfa_gen_fill", "sfa_debug_sm100_scores",
            "sfa_attn_prepare", "sfa_attn_fwd_prepared", "sfa_dist_unique_id", "sfa_dist_init", "sfa_dist_destroy",
            "sfa_dist_staging_bytes", "sfa_dist_allgather_kv", "sfa_dist_unpack_zigzag", "sfa_forward_host_pipelined",
-           "sfa_attn_bwd_workspace_bytes", "sfa_attn_bwd")
+           "sfa_attn_bwd_workspace_bytes", "sfa_attn_bwd", "sfa_attn_fwd_fused_q")
 
 
 def _check(code: int, where: str):
@@ -170,6 +171,27 @@ def attn_fwd(q_idx, q_val, k_idx, k_val, v, *, d, causal=True, scale=None, q_pos
     _check(lib().sfa_attn_fwd(ctypes.byref(desc), _p(q_idx), _p(q_val), _p(k_idx), _p(k_val), _p(v), _p(o),
                               _p(lse), _p(workspace), workspace.numel(), _stream()), "sfa_attn_fwd")
     return o, lse
+
+
+def attn_fwd_fused_q(q, k_idx, k_val, v, *, causal=True, scale=None, q_pos0=0, kernel=KERNEL_AUTO, codes_out=True,
+                     status=None):
+    """Steps 1 (on Q) to 8 in one kernel (include/sfa.h sfa_attn_fwd_fused_q): dense bf16 q, key codes and
+    v -> (O, LSE, q_idx, q_val); the codes are None when codes_out is False."""
+    _dev(q, k_idx, k_val, v)
+    B, H, n_q, d = q.shape
+    _, H_kv, n_kv, k = k_idx.shape
+    desc = make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k, d_v=v.shape[-1], n_q=n_q, n_kv=n_kv, q_pos0=q_pos0,
+                     causal=causal, scale=scale, dtype=_dt(v), kernel=kernel)
+    ws = torch.empty(max(workspace_bytes(desc), 16), dtype=torch.uint8, device=v.device)
+    _check(lib().sfa_attn_prepare(ctypes.byref(desc), _p(k_idx), _p(k_val), _p(v), _p(ws), ws.numel(), _stream()),
+           "sfa_attn_prepare")
+    o = torch.empty((B, H, n_q, v.shape[-1]), dtype=v.dtype, device=v.device)
+    lse = torch.empty((B, H, n_q), dtype=torch.float32, device=v.device)
+    qi = torch.empty((B, H, n_q, k), dtype=torch.uint8, device=v.device) if codes_out else None
+    qv = torch.empty((B, H, n_q, k), dtype=q.dtype, device=v.device) if codes_out else None
+    _check(lib().sfa_attn_fwd_fused_q(ctypes.byref(desc), _p(q), _p(k_idx), _p(k_val), _p(v), _p(o), _p(lse), _p(qi),
+                                      _p(qv), _p(status), _p(ws), ws.numel(), _stream()), "sfa_attn_fwd_fused_q")
+    return o, lse, qi, qv
 
 
 def bucket_keys(k_idx, k_val, *, d, n_q=1, H=None, d_v=64, causal=True, workspace=None):
