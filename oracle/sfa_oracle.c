@@ -38,6 +38,12 @@
  *                    softmax runs over the edges only; a row with no edge gets O = 0, LSE = -inf
  *                    (as A10).
  *
+ *                    window = w > 0 (composition with token sparsity: the causal
+ *                    sliding window of Longformer/Mistral-style local attention, "SFA is
+ *                    orthogonal to token-level sparsity"): key j is allowed only if, in addition,
+ *                      j > q_pos0 + i - w          (the last w positions up to and including i)
+ *                    Rows with no allowed key: O = 0, LSE = -inf (A10).
+ *
  *   ref_scores_row   the s_ij of one row (for the "rows of P sum to 1" pin).
  *
  *   ref_attn_bwd     the backward pass of ref_attn_fwd with the straight-through rule
@@ -148,7 +154,7 @@ int ref_topk_codes(const void *x, int dtype, int64_t rows, int d, int k, uint8_t
 /* ---- attention on the decompressed codes: P:L97-101, P:L43-50 ---------------------- */
 typedef struct {
     int B, H, H_kv, d, k, d_v, causal, dtype, edges_only;
-    int64_t n_q, n_kv, q_pos0;
+    int64_t n_q, n_kv, q_pos0, window;
     double scale;
     const uint8_t *q_idx, *k_idx;
     const void *q_val, *k_val, *v;
@@ -181,15 +187,17 @@ static void attn_one_row(attn_job *J, int64_t flat, double *o, double *lse, doub
     int64_t kvrow0 = ((int64_t)b * J->H_kv + g) * J->n_kv;
     int64_t jmax = J->n_kv - 1;
     if (J->causal && J->q_pos0 + i < jmax) jmax = J->q_pos0 + i; /* A9 */
+    int64_t jmin = 0;
+    if (J->window > 0 && J->q_pos0 + i - J->window + 1 > jmin) jmin = J->q_pos0 + i - J->window + 1; /* N4 window */
     for (int c = 0; c < J->d_v; ++c) o[c] = 0.0;
-    if (jmax < 0) { /* A10 */
+    if (jmax < jmin) { /* A10 */
         *lse = -INFINITY;
         return;
     }
     densify(J->q_idx, J->q_val, J->dtype, flat, J->k, J->d, qd);
     double m = -INFINITY;
     for (int64_t j = 0; j <= jmax; ++j) {
-        if (J->edges_only && !supports_intersect(J->q_idx, flat, J->k_idx, kvrow0 + j, J->k)) {
+        if (j < jmin || (J->edges_only && !supports_intersect(J->q_idx, flat, J->k_idx, kvrow0 + j, J->k))) {
             s[j] = -INFINITY; /* R2: not an edge -> excluded from the softmax */
             continue;
         }
@@ -245,7 +253,8 @@ static void *attn_worker(void *arg) {
 int ref_attn_fwd_ex(int B, int H, int H_kv, int d, int k, int d_v, int64_t n_q, int64_t n_kv, int64_t q_pos0,
                     int causal, double scale, int dtype, const uint8_t *q_idx, const void *q_val,
                     const uint8_t *k_idx, const void *k_val, const void *v, const int64_t *sel, int64_t nsel,
-                    double *o, double *lse, int threads, int edges_only) {
+                    double *o, double *lse, int threads, int edges_only, int64_t window) {
+    if (window < 0) return ORACLE_INVALID_ARGUMENT;
     if (B < 1 || H < 1 || H_kv < 1 || H % H_kv || d < 1 || d > 256 || k < 1 || k > d || d_v < 1 || n_q < 0 ||
         n_kv < 0 || dtype < 0 || dtype > 2 || !(scale > 0) || !isfinite(scale))
         return ORACLE_INVALID_ARGUMENT;
@@ -254,6 +263,7 @@ int ref_attn_fwd_ex(int B, int H, int H_kv, int d, int k, int d_v, int64_t n_q, 
     J.B = B; J.H = H; J.H_kv = H_kv; J.d = d; J.k = k; J.d_v = d_v; J.causal = causal; J.dtype = dtype;
     J.n_q = n_q; J.n_kv = n_kv; J.q_pos0 = q_pos0; J.scale = scale;
     J.edges_only = edges_only != 0;
+    J.window = window;
     J.q_idx = q_idx; J.k_idx = k_idx; J.q_val = q_val; J.k_val = k_val; J.v = v;
     J.sel = sel;
     J.nsel = sel ? nsel : (int64_t)B * H * n_q;
@@ -273,7 +283,7 @@ int ref_attn_fwd(int B, int H, int H_kv, int d, int k, int d_v, int64_t n_q, int
                  const uint8_t *k_idx, const void *k_val, const void *v, const int64_t *sel, int64_t nsel,
                  double *o, double *lse, int threads) {
     return ref_attn_fwd_ex(B, H, H_kv, d, k, d_v, n_q, n_kv, q_pos0, causal, scale, dtype, q_idx, q_val, k_idx,
-                           k_val, v, sel, nsel, o, lse, threads, 0);
+                           k_val, v, sel, nsel, o, lse, threads, 0, 0);
 }
 
 /* s_ij for j = 0..n_kv-1 of one query row (flat id into [B][H][n_q]); masked keys get -inf. */
