@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--config", default="qwen3", choices=sorted(accounting.CONFIGS))
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "sm100", "pair", "wide", "ot"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--window", type=int, default=0,
+                    help="causal sliding window (N4: SFA composed with token sparsity); 0 = full causal")
     ap.add_argument("--edges-only", action="store_true",
                     help="reading A1/R2 (SURVEY 8(f) N4): only pairs whose supports intersect enter the softmax")
     ap.add_argument("--no-e2e", action="store_true")
@@ -199,7 +201,8 @@ def config_of(args, W):
             "global_batch": W.B * args.gpus, "seq_len": W.n, "parallelism": f"weak: batch element r on rank r "
             f"({args.gpus} GPU{'s' if args.gpus > 1 else ''}), no data-path collective",
             "kernel": args.kernel,
-            "semantics": "R2 edges-only (A1/R2)" if getattr(args, "edges_only", False) else "R1 (A1)",
+            "semantics": ("R2 edges-only (A1/R2)" if getattr(args, "edges_only", False) else "R1 (A1)")
+                         + (f", causal sliding window {args.window} (N4)" if getattr(args, "window", 0) else ""),
             "q_topk": "fused into the attention prologue (N3(ii)); stage_ms.attn includes it"
                       if (getattr(args, "fused_q", False) and not getattr(args, "edges_only", False) and W.d_v == 128
                           and W.dtype == "bf16" and args.kernel in ("auto", "ot")) else "own kernel",
@@ -566,7 +569,7 @@ def main():
     sfa.gen_fill(V, seed, inputs.TID_V, offset=rank * V.numel())
     desc = sfa.make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k, d_v=d_v, n_q=n, n_kv=n, causal=W.causal,
                          dtype=sfa.SFA_BF16 if W.dtype == "bf16" else sfa.SFA_F32, kernel=kernel,
-                         edges_only=args.edges_only)
+                         edges_only=args.edges_only, window=args.window)
     q_idx = torch.empty((B, H, n, k), dtype=torch.uint8, device=dev)
     q_val = torch.empty((B, H, n, k), dtype=dt, device=dev)
     k_idx = torch.empty((B, H_kv, n, k), dtype=torch.uint8, device=dev)
@@ -674,7 +677,7 @@ def main():
     # context only (not a step, not a target): dense causal attention on the same shapes through torch's
     # SDPA (FlashAttention/cuDNN backend on B200), bf16 Q, K, V with GQA -- what the codes replace
     context = None
-    if rank == 0 and world == 1 and W.dtype == "bf16" and not args.no_dense_context:
+    if rank == 0 and world == 1 and W.dtype == "bf16" and not args.no_dense_context and not args.window:
         try:
             import torch.nn.functional as F
             qd, kd, vd = Q, K, V
@@ -698,7 +701,7 @@ def main():
 
     pk = peaks()
     attn_ms = stage_ms[3]
-    pairs = B * H * accounting.causal_pairs(n, n, 0, W.causal)
+    pairs = B * H * accounting.causal_pairs(n, n, 0, W.causal, args.window)
     mufu_peak = N_SMS * MUFU_EX2_PER_CLK_SM * pk["sm_max_mhz"] * 1e6  # ex2/s
     achieved = pairs / (attn_ms / 1e3)
     traffic = None  # dram__bytes_read + dram__bytes_write per launch of the attention kernel (ncu --set full)
@@ -750,7 +753,8 @@ def main():
                 "config": config_of(args, W),
                 "stage_ms": {"topk_q": stage_ms[0], "topk_k": stage_ms[1], "prepare": stage_ms[2],
                              "attn": stage_ms[3]},
-                "interactions_per_s": W.expected_interactions / (ms_per_step / 1e3) * world,
+                "interactions_per_s": W.expected_interactions * pairs / (B * H * accounting.causal_pairs(n, n, 0, W.causal))
+                                      / (ms_per_step / 1e3) * world,
                 "pairs_per_s": pairs * world / (ms_per_step / 1e3),
                 "wall_s_timed_region": t_wall,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (5 + int(args.edges_only) - int(fused_q) if sm100 else 4) * args.steps,

@@ -105,6 +105,11 @@ typedef struct {
                             a feature index (zero-valued selected entries count, A8); a row with no edge
                             gets O = 0, LSE = -inf.  R2 runs on SM100_OT (bf16, d_v = 128) and SIMT
                             (AUTO picks them); other explicit kernels -> SFA_ERR_UNSUPPORTED.          */
+    int64_t window;      /* 0: off.  > 0 (requires causal = 1): causal sliding window -- SFA composed with
+                            token-level sparsity: key j is allowed only if
+                            also j > q_pos0 + i - window.  Key tiles before a query block's window are
+                            skipped, so the work is ~ n * window.  Runs on SM100_OT and SIMT (AUTO picks
+                            them); DECODE / SM100 / PAIR / WIDE and the backward -> SFA_ERR_UNSUPPORTED. */
 } sfa_attn_desc;
 
 /* Bytes of device workspace sfa_attn_fwd needs (0 on an invalid desc):

@@ -8,10 +8,13 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 
-def causal_pairs(n_q: int, n_kv: int, q_pos0: int = 0, causal: bool = True) -> int:
-    """Allowed (query, key) pairs of one head: sum_i min(n_kv, q_pos0 + i + 1)."""
+def causal_pairs(n_q: int, n_kv: int, q_pos0: int = 0, causal: bool = True, window: int = 0) -> int:
+    """Allowed (query, key) pairs of one head: sum_i min(n_kv, q_pos0 + i + 1); with a causal sliding
+    window w > 0 (N4) key j also needs j > q_pos0 + i - w."""
     if not causal:
         return n_q * n_kv
+    if window > 0:
+        return sum(max(0, min(n_kv - 1, q_pos0 + i) - max(0, q_pos0 + i - window + 1) + 1) for i in range(n_q))
     tot = 0
     # rows whose window is still growing: q_pos0 + i + 1 <= n_kv
     grow = max(0, min(n_q, n_kv - q_pos0))

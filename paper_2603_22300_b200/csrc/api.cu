@@ -39,6 +39,10 @@ sfa_status validate_desc(const sfa_attn_desc *d) {
         return SFA_ERR_UNSUPPORTED;
     if ((d->n_kv + 63) / 64 > (int64_t)INT32_MAX) return SFA_ERR_UNSUPPORTED;
     if (d->edges_only != 0 && d->edges_only != 1) return SFA_ERR_INVALID_ARGUMENT;
+    if (d->window < 0 || (d->window > 0 && !d->causal)) return SFA_ERR_INVALID_ARGUMENT;
+    if (d->window > 0 && d->kernel != SFA_KERNEL_AUTO && d->kernel != SFA_KERNEL_SIMT &&
+        d->kernel != SFA_KERNEL_SM100_OT)
+        return SFA_ERR_UNSUPPORTED;  // the window is built into the OT and SIMT kernels only
     if (d->edges_only && d->kernel != SFA_KERNEL_AUTO && d->kernel != SFA_KERNEL_SIMT &&
         d->kernel != SFA_KERNEL_SM100_OT)
         return SFA_ERR_UNSUPPORTED;  // R2 is built into the OT and SIMT kernels only
@@ -55,7 +59,7 @@ BucketLayout layout_of(const sfa_attn_desc *d) {
 int resolve_kernel(const sfa_attn_desc *d) {
     if (d->kernel == SFA_KERNEL_SIMT || d->dtype == SFA_F32) return SFA_KERNEL_SIMT;
     if (d->kernel != SFA_KERNEL_AUTO) return d->kernel;
-    if (d->edges_only) return d->d_v == 128 ? SFA_KERNEL_SM100_OT : SFA_KERNEL_SIMT;  // R2 kernels
+    if (d->edges_only || d->window > 0) return d->d_v == 128 ? SFA_KERNEL_SM100_OT : SFA_KERNEL_SIMT;  // R2 / window
     if ((int64_t)(d->H / d->H_kv) * d->n_q <= 16) return SFA_KERNEL_DECODE;
     return d->d_v == 128 ? SFA_KERNEL_SM100_OT : SFA_KERNEL_SM100;
 }
@@ -114,6 +118,7 @@ AttnParams make_params(const sfa_attn_desc *d, const uint8_t *q_idx, const void 
     p.scale_log2 = d->scale * kLog2e;
     p.L = layout_of(d);
     p.edges_only = d->edges_only;
+    p.window = d->window;
     p.kfmask = (ws && uses_kmask(d)) ? (const uint32_t *)((const uint8_t *)ws + align_up(vprep_bytes(d), 256)) : nullptr;
     return p;
 }
@@ -164,7 +169,7 @@ bool codes_aligned(const void *a, const void *b) { return aligned16(a) && aligne
 
 // the fused step-1-on-Q path (N3(ii)) exists for the SM100_OT kernel with R1 semantics
 bool fusable(const sfa_attn_desc *d) {
-    return d->dtype == SFA_BF16 && !d->edges_only && resolve_kernel(d) == SFA_KERNEL_SM100_OT;
+    return d->dtype == SFA_BF16 && !d->edges_only && d->window == 0 && resolve_kernel(d) == SFA_KERNEL_SM100_OT;
 }
 
 }  // namespace
@@ -302,7 +307,7 @@ sfa_status sfa_attn_bwd(const sfa_attn_desc *desc, const uint8_t *q_idx, const v
                         sfa_stream_t stream) {
     sfa_status s = validate_desc(desc);
     if (s != SFA_OK) return s;
-    if (desc->dtype != SFA_BF16) return SFA_ERR_UNSUPPORTED;
+    if (desc->dtype != SFA_BF16 || desc->edges_only || desc->window > 0) return SFA_ERR_UNSUPPORTED;
     if (!q_idx || !q_val || !k_idx || !k_val || !v || !o || !lse || !dO || !dq_val || !dk_val || !dv || !workspace)
         return SFA_ERR_INVALID_ARGUMENT;
     if (!aligned16(v) || !aligned16(o) || !aligned16(dO) || !aligned16(dv) || !aligned16(workspace) ||

@@ -66,7 +66,13 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const AttnParams p) {
 #pragma unroll
     for (int c = 0; c < DV; ++c) O[c] = 0.f;
 
-    for (int t = 0; t < ntiles; ++t) {
+    int t0 = 0;  // N4 sliding window: key tiles before the window of the block's first row are skipped
+    if (p.window > 0) {
+        const int64_t kb = p.q_pos0 + (int64_t)qb * 128 - p.window + 1;
+        if (kb > 0) t0 = (int)(kb / BK);
+        if (t0 > ntiles - 1) t0 = ntiles - 1 < 0 ? 0 : ntiles - 1;
+    }
+    for (int t = t0; t < ntiles; ++t) {
         __syncthreads();
         {  // stage bucket tile and V tile
             const uint8_t *tb = tiles + (int64_t)t * p.L.tile_bytes;
@@ -113,9 +119,14 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const AttnParams p) {
             int64_t jv = p.n_kv - key0;
             if (p.causal && p.q_pos0 + r - key0 + 1 < jv) jv = p.q_pos0 + r - key0 + 1;
             if (jv > BK) jv = BK;
+            int jl = 0;  // first key of the window in this tile
+            if (p.window > 0) {
+                const int64_t lo = p.q_pos0 + r - p.window + 1 - key0;
+                jl = lo < 0 ? 0 : (lo > BK ? BK : (int)lo);
+            }
             // step 6: online softmax (log2 domain)
             float mx = -INFINITY;
-            for (int j = 0; j < jv; ++j) {
+            for (int j = jl; j < jv; ++j) {
                 const float sj = slab[j * 32];
                 if (!EDGE || __float_as_uint(sj) != UNTOUCHED) mx = fmaxf(mx, sj);
             }
@@ -130,7 +141,7 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(const AttnParams p) {
             for (int j = 0; j < BK; ++j) {
                 const float s = slab[j * 32];
                 slab[j * 32] = slab_init;
-                if (j < jv && (!EDGE || __float_as_uint(s) != UNTOUCHED)) {
+                if (j >= jl && j < jv && (!EDGE || __float_as_uint(s) != UNTOUCHED)) {
                     const float pj = fast_exp2(s - m);
                     l += pj;
                     const T *vr = Vs + j * DV;

@@ -145,7 +145,8 @@ __device__ __forceinline__ void prefetch_l1(const void *ptr) {
 // of tile t loads the DENSE bf16 Q row, selects its top-k with the same code as the stand-alone kernel
 // (topk_row.cuh), writes the masked row straight into the swizzled Q~ tile and (optionally) the row's
 // code to q_idx_out / q_val_out; the decompression warps then only build K~.
-template <int D, bool DBG, bool EDGE, bool FUSEQ>
+// WIN: causal sliding window (N4) -- a template flag so the full-causal kernel carries none of its work.
+template <int D, bool DBG, bool EDGE, bool FUSEQ, bool WIN>
 __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid_constant__ CUtensorMap tmap_v,
                                                                       const OtArgs a) {
     using C = Cfg<D>;
@@ -172,6 +173,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         const int64_t lim = (p.q_pos0 + last) / BN + 1;
         if (lim < nt) nt = (int)lim;
     }
+    // sliding window (N4): key tiles before the window of the CTA's first row are skipped; every loop
+    // below runs over the nt tiles j0, j0 + 1, ... (j relative, key tile j0 + j)
+    int j0r = 0;
+    if (WIN) {
+        const int64_t kb = p.q_pos0 + (int64_t)tl[0].qb * BM - p.window + 1;
+        if (kb > 0) j0r = (int)(kb / BN);
+        if (j0r > nt - 1) j0r = nt - 1;  // no key left: one fully masked tile (O = 0, LSE = -inf)
+        nt -= j0r;
+    }
+    const int j0 = WIN ? j0r : 0;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NBAR; ++i) {
@@ -203,6 +214,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         const bool row_ok = tl[t].valid && i < p.n_q;
         int64_t kend = p.n_kv;
         if (p.causal && p.q_pos0 + i + 1 < kend) kend = p.q_pos0 + i + 1;
+        const int64_t kbeg = WIN ? p.q_pos0 + i - p.window + 1 : 0;  // N4 sliding window
         const float cs = a.c_scale;
         if (FUSEQ) {
             // ---- step 1 on this row: dense Q row -> top-k masks -> masked row into the Q~ tile
@@ -297,11 +309,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         if (EDGE && lane < 2 * (D / 16)) prefetch_l1(kf_head + lane * 8);  // tile 0: D x 16 bytes of bitsets
         float m = -INFINITY, l = 0.f;
         for (int j = 0; j < nt; ++j) {
-            int64_t lim64 = kend - (int64_t)j * BN;
+            int64_t lim64 = kend - (int64_t)(j0 + j) * BN;
             const int lim = lim64 < 0 ? 0 : (lim64 > BN ? BN : (int)lim64);
+            int lo = 0;  // first allowed key of the window in this tile
+            if (WIN) {
+                const int64_t lo64 = kbeg - (int64_t)(j0 + j) * BN;
+                lo = lo64 < 0 ? 0 : (lo64 > BN ? BN : (int)lo64);
+            }
             uint32_t eh[4];
             if (EDGE) {
-                const uint4 *kf = kf_head + (int64_t)j * D;
+                const uint4 *kf = kf_head + (int64_t)(j0 + j) * D;
                 uint4 h = make_uint4(0u, 0u, 0u, 0u);
                 if (row_ok && p.k <= 16) {
 #pragma unroll
@@ -330,7 +347,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int rem = lim - 32 * q;  // step 5 folded in: keys at or past lim are excluded
-                    eh[q] = hw[q] & (rem >= 32 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : ((1u << rem) - 1u)));
+                    const int rlo = lo - 32 * q;   // and keys before the window
+                    eh[q] = hw[q] & (rem >= 32 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : ((1u << rem) - 1u))) &
+                            (rlo <= 0 ? 0xFFFFFFFFu : (rlo >= 32 ? 0u : ~((1u << rlo) - 1u)));
                 }
             }
             mbar_wait(BAR(SFULL + t), j & 1);
@@ -375,13 +394,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
 #pragma unroll
                     for (int c = 0; c < 32; ++c) a.dbg[r * BN + 32 * q + c] = __uint_as_float(s[q][c]);
             }
-            if (!EDGE && lim < BN) {  // step 5 on diagonal / ragged tiles: excluded keys -> -inf -> p = 0
+            if (!EDGE && (lim < BN || (WIN && lo > 0))) {  // step 5 on diagonal / ragged / window-edge tiles: excluded -> -inf
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     mq[q] = -INFINITY;
 #pragma unroll
                     for (int c = 0; c < 32; ++c) {
-                        if (32 * q + c >= lim) s[q][c] = 0xFF800000u;
+                        if (32 * q + c >= lim || 32 * q + c < lo) s[q][c] = 0xFF800000u;
                         mq[q] = fmaxf(mq[q], __uint_as_float(s[q][c]));
                     }
                 }
@@ -511,7 +530,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         const int64_t kv0 = ((int64_t)b * p.H_kv + g) * p.n_kv;
         for (int j = 0; j < nt; ++j) {
             const int s = j % C::NK, u = j / C::NK;
-            const int64_t key = (int64_t)j * BN + r;
+            const int64_t key = (int64_t)(j0 + j) * BN + r;
             const bool ok = key < p.n_kv;
             mbar_wait(BAR(KEMPTY + s), (u & 1) ^ 1);
             densify_row<D>(sbase + C::OFF_K + s * C::KT, BN, r, ok, p.k_idx + (kv0 + key) * k, kv + (kv0 + key) * k, k);
@@ -594,7 +613,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                     const uint32_t dst = sbase + C::OFF_V + vs * C::VT;
 #pragma unroll
                     for (int cb = 0; cb < DV / 64; ++cb)
-                        tma_load_3d(dst + cb * BN * 128, &tmap_v, BAR(VFULL + vs), cb * 64, j * BN, bhkv);
+                        tma_load_3d(dst + cb * BN * 128, &tmap_v, BAR(VFULL + vs), cb * 64, (j0 + j) * BN, bhkv);
                 }
             }
             __syncwarp();
@@ -637,11 +656,14 @@ cudaError_t launch_t(const OtArgs &a, cudaStream_t stream, int items) {
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    auto kern = p.q_dense != nullptr ? attn_sm100_ot_kernel<D, false, false, true>
-                : p.edges_only ? (a.dbg != nullptr ? attn_sm100_ot_kernel<D, true, true, false>
-                                                   : attn_sm100_ot_kernel<D, false, true, false>)
-                               : (a.dbg != nullptr ? attn_sm100_ot_kernel<D, true, false, false>
-                                                   : attn_sm100_ot_kernel<D, false, false, false>);
+    const bool win = p.window > 0;
+    auto kern = p.q_dense != nullptr ? attn_sm100_ot_kernel<D, false, false, true, false>
+                : win ? (p.edges_only ? attn_sm100_ot_kernel<D, false, true, false, true>
+                                      : attn_sm100_ot_kernel<D, false, false, false, true>)
+                : p.edges_only ? (a.dbg != nullptr ? attn_sm100_ot_kernel<D, true, true, false, false>
+                                                   : attn_sm100_ot_kernel<D, false, true, false, false>)
+                               : (a.dbg != nullptr ? attn_sm100_ot_kernel<D, true, false, false, false>
+                                                   : attn_sm100_ot_kernel<D, false, false, false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     kern<<<items, NTHREADS, C::SMEM, stream>>>(tm, a);
@@ -653,7 +675,8 @@ cudaError_t launch_t(const OtArgs &a, cudaStream_t stream, int items) {
 cudaError_t launch_attn_sm100_ot(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg) {
     if ((d != 64 && d != 128) || d_v != DV) return cudaErrorNotSupported;
     if (p.edges_only && p.kfmask == nullptr) return cudaErrorInvalidValue;
-    if (p.q_dense != nullptr && (p.edges_only || dbg != nullptr)) return cudaErrorNotSupported;
+    if (p.q_dense != nullptr && (p.edges_only || dbg != nullptr || p.window > 0)) return cudaErrorNotSupported;
+    if (p.window > 0 && dbg != nullptr) return cudaErrorNotSupported;
     OtArgs a;
     a.p = p;
     a.nqb = (int)((p.n_q + BM - 1) / BM);

@@ -21,6 +21,7 @@ struct AttnParams {
     float scale_log2;  // scale * log2(e): logits live in the log2 domain inside the kernels
     BucketLayout L;
     int32_t edges_only;      // reading A1/R2: only pairs whose supports intersect enter the softmax
+    int64_t window = 0;      // N4: causal sliding window, key j also needs j > q_pos0 + i - window (0 = off)
     const uint32_t *kfmask;  // R2, SM100_OT: per key tile, per feature, the 128-bit set of keys selecting it
     // fused step 1 on Q (SM100_OT, N3(ii)): dense bf16 Q [B][H][n_q][d] instead of q codes; the kernel
     // optionally writes the codes it selected (q_idx_out / q_val_out) and flags non-finite Q

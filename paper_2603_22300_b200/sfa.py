@@ -34,7 +34,7 @@ class AttnDesc(ctypes.Structure):
                 ("d", ctypes.c_int32), ("k", ctypes.c_int32), ("d_v", ctypes.c_int32),
                 ("n_q", ctypes.c_int64), ("n_kv", ctypes.c_int64), ("q_pos0", ctypes.c_int64),
                 ("causal", ctypes.c_int32), ("scale", ctypes.c_float), ("dtype", ctypes.c_int32),
-                ("kernel", ctypes.c_int32), ("edges_only", ctypes.c_int32)]
+                ("kernel", ctypes.c_int32), ("edges_only", ctypes.c_int32), ("window", ctypes.c_int64)]
 
 
 _lib = None
@@ -118,12 +118,13 @@ def _dev(*ts):
 
 
 def make_desc(*, B, H, H_kv, d, k, d_v, n_q, n_kv, q_pos0=0, causal=True, scale=None, dtype=SFA_BF16,
-              kernel=KERNEL_AUTO, edges_only=False) -> AttnDesc:
-    """edges_only: reading A1/R2 (include/sfa.h) -- only pairs whose supports intersect."""
+              kernel=KERNEL_AUTO, edges_only=False, window=0) -> AttnDesc:
+    """edges_only: reading A1/R2 (include/sfa.h) -- only pairs whose supports intersect.
+    window > 0: causal sliding window (N4) -- key j also needs j > q_pos0 + i - window."""
     if scale is None:
         scale = 1.0 / math.sqrt(d)  # P:L99, reading A5
     return AttnDesc(B, H, H_kv, d, k, d_v, n_q, n_kv, q_pos0, int(bool(causal)), scale, dtype, kernel,
-                    int(bool(edges_only)))
+                    int(bool(edges_only)), int(window))
 
 
 def topk_codes(x: torch.Tensor, k: int, status: torch.Tensor | None = None):
@@ -138,11 +139,11 @@ def topk_codes(x: torch.Tensor, k: int, status: torch.Tensor | None = None):
     return idx, val
 
 
-def _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, kernel, dtype, edges_only=False):
+def _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, kernel, dtype, edges_only=False, window=0):
     B, H, n_q, k = q_idx.shape
     _, H_kv, n_kv, _ = k_idx.shape
     return make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k, d_v=v.shape[-1], n_q=n_q, n_kv=n_kv, q_pos0=q_pos0,
-                     causal=causal, scale=scale, dtype=dtype, kernel=kernel, edges_only=edges_only)
+                     causal=causal, scale=scale, dtype=dtype, kernel=kernel, edges_only=edges_only, window=window)
 
 
 def workspace_bytes(desc: AttnDesc) -> int:
@@ -154,11 +155,11 @@ def key_tile(desc: AttnDesc) -> int:
 
 
 def attn_fwd(q_idx, q_val, k_idx, k_val, v, *, d, causal=True, scale=None, q_pos0=0, kernel=KERNEL_AUTO,
-             workspace=None, out=None, edges_only=False):
+             workspace=None, out=None, edges_only=False, window=0):
     """Stage 2: (O, LSE) = FlashSFA forward over the codes (bucketing + attention kernels).
     edges_only: reading A1/R2 -- only the pairs whose supports intersect enter the softmax."""
     _dev(q_idx, q_val, k_idx, k_val, v)
-    desc = _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, kernel, _dt(v), edges_only)
+    desc = _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, kernel, _dt(v), edges_only, window)
     B, H, n_q, _ = q_idx.shape
     nb = workspace_bytes(desc)
     if workspace is None:
@@ -265,13 +266,13 @@ def scratch_bytes(desc: AttnDesc) -> int:
 
 
 def forward(q, k, v, *, k_code, causal=True, scale=None, q_pos0=0, kernel=KERNEL_AUTO, scratch=None, out=None,
-            edges_only=False):
+            edges_only=False, window=0):
     """The whole hot path (stage 1 on Q and K, then stage 2): dense q, k, v -> (O, LSE)."""
     _dev(q, k, v)
     B, H, n_q, d = q.shape
     _, H_kv, n_kv, _ = k.shape
     desc = make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k_code, d_v=v.shape[-1], n_q=n_q, n_kv=n_kv, q_pos0=q_pos0,
-                     causal=causal, scale=scale, dtype=_dt(v), kernel=kernel, edges_only=edges_only)
+                     causal=causal, scale=scale, dtype=_dt(v), kernel=kernel, edges_only=edges_only, window=window)
     if scratch is None:
         scratch = torch.empty(max(scratch_bytes(desc), 16), dtype=torch.uint8, device=v.device)
     if out is None:
