@@ -247,9 +247,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
             }
 #pragma unroll
             for (int q = 0; q < NW; ++q) ab[q] = raw[q] & 0x7FFF7FFFu;
-            if (row_ok && p.status_word != nullptr && tk::row_max_key(ab) >= 0x7F80u) atomicOr(p.status_word, 1u);
+            const uint32_t mx = tk::row_max_key(ab);
+            if (row_ok && p.status_word != nullptr && mx >= 0x7F80u) atomicOr(p.status_word, 1u);
             uint32_t gm[D / 32];
-            tk::select_masks(ab, p.k, gm);
+            tk::select_masks(ab, p.k, gm, mx);
             if (!row_ok) {
 #pragma unroll
                 for (int w = 0; w < D / 32; ++w) gm[w] = 0u;

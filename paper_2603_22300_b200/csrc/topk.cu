@@ -157,11 +157,12 @@ __global__ void __launch_bounds__(TK_ROWS) topk_rows_bf16_kernel(const uint16_t 
         ab[4 * c + 2] = w.z & 0x7FFF7FFFu;
         ab[4 * c + 3] = w.w & 0x7FFF7FFFu;
     }
-    if (active && tk::row_max_key(ab) >= 0x7F80u && status_word != nullptr) atomicOr(status_word, 1u);
+    const uint32_t mx = tk::row_max_key(ab);
+    if (active && mx >= 0x7F80u && status_word != nullptr) atomicOr(status_word, 1u);
     // 3-4. threshold search and selection masks (topk_row.cuh)
     constexpr int NM = D / 32;
     uint32_t gm[NM];
-    tk::select_masks(ab, k, gm);
+    tk::select_masks(ab, k, gm, mx);
     // 5. ascending compaction into the staging area (values re-read from the row in shared memory)
     uint8_t *my_i = oidx + t * k;
     uint16_t *my_v = oval + t * k;

@@ -43,13 +43,20 @@ __device__ __forceinline__ uint32_t row_max_key(const uint32_t (&ab)[NW]) {
     return max(mx2 & 0xFFFFu, mx2 >> 16);
 }
 
+// mx: the row's max key (row_max_key).  T is found exponent first: walking down from the max key's
+// exponent, the first exponent e with #{key >= e.2^7} >= k is T's (the count is monotone in the
+// threshold), typically one or two passes since the top k of a row sit within a binade or two of its
+// max; then the 7 mantissa bits by bisection -- ~9 counting passes instead of 15.
 template <int NW>
-__device__ __forceinline__ void select_masks(const uint32_t (&ab)[NW], int k, uint32_t (&gm)[NW / 16]) {
+__device__ __forceinline__ void select_masks(const uint32_t (&ab)[NW], int k, uint32_t (&gm)[NW / 16], uint32_t mx) {
     constexpr int NM = NW / 16;
     // largest T with #{key >= T} >= k
-    uint32_t T = 0;
+    int e = (int)((mx > 0x7FFFu ? 0x7FFFu : mx) >> 7);
 #pragma unroll 1
-    for (int bit = 14; bit >= 0; --bit) {
+    while (e > 0 && count_ge(ab, (uint32_t)e << 7) < k) --e;
+    uint32_t T = (uint32_t)e << 7;
+#pragma unroll 1
+    for (int bit = 6; bit >= 0; --bit) {
         const uint32_t cand = T | (1u << bit);
         if (count_ge(ab, cand) >= k) T = cand;
     }
