@@ -100,8 +100,35 @@ struct Tile {
     bool valid;
 };
 
+// Work-item order.  SFA_OT_ORDER 1 (default): kv-group major -- all work items of one (batch, kv head)
+// group run back to back (heaviest causal query blocks of the group first), so the ~148 resident CTAs
+// share one group's K codes and V in L2 instead of streaming all groups' at once.  0: query-block
+// major across every head (global LPT order, the earlier version).
+#ifndef SFA_OT_ORDER
+#define SFA_OT_ORDER 1
+#endif
 __device__ __forceinline__ void decode_item(const OtArgs &a, int item, int &b, Tile (&t)[2]) {
     const AttnParams &p = a.p;
+#if SFA_OT_ORDER
+    if (a.pair_heads) {
+        const int PG = p.H / p.H_kv / 2;  // head pairs per kv group
+        const int per_g = PG * a.nqb;
+        const int gi = item / per_g, rem = item % per_g;
+        const int qb = a.nqb - 1 - rem / PG, pl = rem % PG;
+        b = gi / p.H_kv;
+        const int h0 = 2 * ((gi % p.H_kv) * PG + pl);
+        t[0] = {h0, qb, true};
+        t[1] = {h0 + 1, qb, true};
+    } else {
+        const int npairs = (a.nqb + 1) / 2;
+        const int bh = item / npairs, pr = npairs - 1 - item % npairs;
+        b = bh / p.H;
+        const int h = bh % p.H;
+        t[0] = {h, 2 * pr, 2 * pr < a.nqb};
+        t[1] = {h, 2 * pr + 1, 2 * pr + 1 < a.nqb};
+    }
+    return;
+#endif
     const int rank = item / a.per_rank, rest = item % a.per_rank;
     if (a.pair_heads) {
         const int qb = a.nqb - 1 - rank;  // heaviest causal blocks first (LPT)
