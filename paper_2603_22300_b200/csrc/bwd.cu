@@ -114,9 +114,13 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
 #define BAR(i) (sb + C::OFF_BAR + 8u * (uint32_t)(i))
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gb + C::OFF_BAR + 200);
 
-    const int bh_n = a.B * a.H;
-    const int ib = a.nqb - 1 - (int)(blockIdx.x / bh_n);  // heaviest causal tiles first
-    const int bh = (int)(blockIdx.x % bh_n), b = bh / a.H, h = bh % a.H, g = h / (a.H / a.H_kv);
+    // kv-group-major order (as the forward): the group's R heads x query tiles, heaviest causal tiles first,
+    // so resident CTAs share one group's K codes and V in L2
+    const int Rg = a.H / a.H_kv;
+    const int per_g = Rg * a.nqb;
+    const int gi = (int)(blockIdx.x / per_g), rem = (int)(blockIdx.x % per_g);
+    const int ib = a.nqb - 1 - rem / Rg;
+    const int b = gi / a.H_kv, g = gi % a.H_kv, h = g * Rg + rem % Rg;
     int nt = a.nkt;
     if (a.causal) {
         int64_t last = (int64_t)ib * BM + BM - 1;
@@ -360,9 +364,10 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gb + C::OFF_BAR + 200);
     float *ldv = reinterpret_cast<float *>(gb + C::OFF_LD);  // [stage][{lse2, D}][128]
 
-    const int bg_n = a.B * a.H_kv;
-    const int jb = (int)(blockIdx.x / bg_n);  // low key tiles see the most query tiles: first
-    const int bg = (int)(blockIdx.x % bg_n), b = bg / a.H_kv, g = bg % a.H_kv;
+    // kv-group-major order: one group's key tiles back to back, low key tiles (most query tiles) first,
+    // so resident CTAs share the group's query codes and dO in L2
+    const int bg = (int)(blockIdx.x / a.nkt), jb = (int)(blockIdx.x % a.nkt);
+    const int b = bg / a.H_kv, g = bg % a.H_kv;
     const int R = a.H / a.H_kv;
     int ib0 = 0;
     if (a.causal) {  // first query tile holding a query at or after this tile's first key
