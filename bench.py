@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--edges-only", action="store_true",
                     help="reading A1/R2 (SURVEY 8(f) N4): only pairs whose supports intersect enter the softmax")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--concurrent-stages", action="store_true",
+                    help="stage 1 on K and step 3 on a second stream concurrently with stage 1 on Q (measured: no "
+                         "gain, the top-k kernels compete for the SMs); default: back to back on one stream")
     ap.add_argument("--no-dense-context", action="store_true", help="skip the dense SDPA context timing")
     ap.add_argument("--fused-q", action="store_true",
                     help="step 1 on Q inside the attention prologue (sfa_attn_fwd_fused_q, N3(ii) ablation)")
@@ -588,15 +591,38 @@ def main():
     fused_q = (W.dtype == "bf16" and d_v == 128 and args.kernel in ("auto", "ot") and not args.edges_only
                and args.fused_q)
 
+    # the key path (stage 1 on K, step 3) is independent of stage 1 on Q: it runs on a second stream and
+    # joins before the attention with --concurrent-stages (default: one stream, the stages back to back)
+    s2 = torch.cuda.Stream(device=dev)
+    kev = {}
+
     def step(ev=None):
         # stage 1 on Q, stage 1 on K, step 3 (V prep for sm100 / buckets for simt), steps 4-8 attention
         if ev: ev[0].record()
-        r1 = 0 if fused_q else L.sfa_topk_codes(P(Q), dcode, B * H * n, d, d, k, P(q_idx), P(q_val), P(status), st())
-        if ev: ev[1].record()
-        r2 = L.sfa_topk_codes(P(K), dcode, B * H_kv * n, d, d, k, P(k_idx), P(k_val), P(status), st())
-        if ev: ev[2].record()
-        r3 = L.sfa_attn_prepare(ctypes.byref(desc), P(k_idx), P(k_val), P(V), P(ws), ws.numel(), st())
-        if ev: ev[3].record()
+        if not args.concurrent_stages:
+            r1 = 0 if fused_q else L.sfa_topk_codes(P(Q), dcode, B * H * n, d, d, k, P(q_idx), P(q_val), P(status), st())
+            if ev: ev[1].record()
+            r2 = L.sfa_topk_codes(P(K), dcode, B * H_kv * n, d, d, k, P(k_idx), P(k_val), P(status), st())
+            if ev: ev[2].record()
+            r3 = L.sfa_attn_prepare(ctypes.byref(desc), P(k_idx), P(k_val), P(V), P(ws), ws.numel(), st())
+            if ev: ev[3].record()
+        else:
+            fork = torch.cuda.Event()
+            fork.record()
+            s2.wait_event(fork)
+            with torch.cuda.stream(s2):
+                if ev: kev[id(ev)][0].record()
+                r2 = L.sfa_topk_codes(P(K), dcode, B * H_kv * n, d, d, k, P(k_idx), P(k_val), P(status), st())
+                if ev: kev[id(ev)][1].record()
+                r3 = L.sfa_attn_prepare(ctypes.byref(desc), P(k_idx), P(k_val), P(V), P(ws), ws.numel(), st())
+                if ev: kev[id(ev)][2].record()
+                join = torch.cuda.Event()
+                join.record()
+            r1 = 0 if fused_q else L.sfa_topk_codes(P(Q), dcode, B * H * n, d, d, k, P(q_idx), P(q_val), P(status), st())
+            if ev: ev[1].record()
+            torch.cuda.current_stream().wait_event(join)
+            if ev: ev[2].record()
+            if ev: ev[3].record()
         if fused_q:  # step 1 on Q inside the attention prologue (N3(ii)); the q codes are still written out
             r4 = L.sfa_attn_fwd_fused_q(ctypes.byref(desc), P(Q), P(k_idx), P(k_val), P(V), P(O), P(LSE), P(q_idx),
                                         P(q_val), P(status), P(ws), ws.numel(), st())
@@ -612,6 +638,8 @@ def main():
         step()
     torch.cuda.synchronize()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    for e in evs:
+        kev[id(e)] = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -628,6 +656,11 @@ def main():
     step_ms = [sum(p) for p in per]
     tot_ms = sum(step_ms)
     stage_ms = [sum(p[j] for p in per) / args.steps for j in range(4)]
+    join_wait_ms = None
+    if args.concurrent_stages:  # key path timed on its own stream; [1] + [2] of `per` are the join wait
+        join_wait_ms = stage_ms[1] + stage_ms[2]
+        stage_ms[1] = sum(kev[id(e)][0].elapsed_time(kev[id(e)][1]) for e in evs) / args.steps
+        stage_ms[2] = sum(kev[id(e)][1].elapsed_time(kev[id(e)][2]) for e in evs) / args.steps
     if world > 1:
         t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -752,7 +785,10 @@ def main():
                 "data": "synthetic (seeded counter-based generator on device, DESIGN.md input recipe)",
                 "config": config_of(args, W),
                 "stage_ms": {"topk_q": stage_ms[0], "topk_k": stage_ms[1], "prepare": stage_ms[2],
-                             "attn": stage_ms[3]},
+                             "attn": stage_ms[3],
+                             "note": ("topk_k and prepare run on a second stream concurrently with topk_q; the step "
+                                      f"waited {join_wait_ms:.4f} ms for them after topk_q")
+                             if join_wait_ms is not None else "stages back to back on one stream"},
                 "interactions_per_s": W.expected_interactions * pairs / (B * H * accounting.causal_pairs(n, n, 0, W.causal))
                                       / (ms_per_step / 1e3) * world,
                 "pairs_per_s": pairs * world / (ms_per_step / 1e3),
