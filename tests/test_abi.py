@@ -101,3 +101,30 @@ def test_bucketed_entry_points_need_simt(sfa):
     d = desc(sfa, kernel=sfa.KERNEL_SM100)
     assert L.sfa_bucket_keys(ctypes.byref(d), *([ctypes.c_void_p(16)] * 3), 1 << 30, None) == 3
     assert L.sfa_attn_fwd_bucketed(ctypes.byref(d), *([ctypes.c_void_p(16)] * 6), 1 << 30, None) == 3
+
+
+def test_n4_semantics_validation(sfa):
+    """edges_only (R2) and window (sliding window) are validated on the host before any launch and
+    select the OT / SIMT kernels; the R2 workspace adds the per-tile feature bitsets (edges.cu)."""
+    L = sfa.lib()
+    base = L.sfa_attn_workspace_bytes(ctypes.byref(desc(sfa)))
+    r2 = L.sfa_attn_workspace_bytes(ctypes.byref(desc(sfa, edges_only=True)))
+    ntiles = (300 + 127) // 128
+    assert r2 == (base + 255) // 256 * 256 + 1 * 2 * ntiles * 128 * 16  # [B*H_kv][tiles][d][4] u32
+    assert L.sfa_attn_workspace_bytes(ctypes.byref(desc(sfa, window=64))) == base  # window: no extra state
+    for b in (dict(window=-1), dict(window=16, causal=False)):
+        d = desc(sfa, **b)
+        assert L.sfa_attn_fwd(ctypes.byref(d), *([ctypes.c_void_p(16)] * 8), 1 << 30, None) == 1, b
+    for kern in (sfa.KERNEL_SM100, sfa.KERNEL_SM100_PAIR, sfa.KERNEL_SM100_WIDE, sfa.KERNEL_DECODE):
+        for b in (dict(edges_only=True), dict(window=16)):
+            d = desc(sfa, kernel=kern, **b)
+            assert L.sfa_attn_fwd(ctypes.byref(d), *([ctypes.c_void_p(16)] * 8), 1 << 30, None) == 3, (kern, b)
+    # the fused step-1-on-Q entry needs the OT kernel with R1 and no window
+    for b in (dict(edges_only=True), dict(window=16), dict(d_v=64)):
+        d = desc(sfa, **b)
+        assert L.sfa_attn_fwd_fused_q(ctypes.byref(d), *([ctypes.c_void_p(16)] * 9), ctypes.c_void_p(16),
+                                      1 << 30, None) == 3, b
+    # the backward covers R1 without a window
+    for b in (dict(edges_only=True), dict(window=16)):
+        d = desc(sfa, **b)
+        assert L.sfa_attn_bwd(ctypes.byref(d), *([ctypes.c_void_p(16)] * 12), 1 << 30, None) == 3, b
