@@ -4,10 +4,13 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config qwen3] [--kernel auto|simt|sm100]
     python bench.py --impl reference ...      # the fp64 CPU oracle on this box's host cores
 
-One step = one pass of the whole hot path over one batch element of the
-workload: top-k codes of Q and of K (stage 1), key-tile bucketing, FlashSFA attention (stage 2),
-inputs resident in HBM.  Weak scaling: rank r owns batch element r of a B=N batch (independent
-problems, no data-path collective).  Rank 0 prints ONE JSON line.
+One step = one pass of the whole hot path over the workload: top-k codes of Q
+and of K (stage 1), the key-side preparation (step 3), FlashSFA attention (stage 2), inputs resident
+in HBM.  Multi-GPU (one process per GPU; `--gpus N` re-launches itself under torch.distributed.run
+when no launcher set WORLD_SIZE): the config's problem is split by (batch, kv head) units over the
+ranks (SURVEY 8(e)-1, strong scaling, no data-path collective), and the `long_context` block of the
+same line runs one 128K-token sequence query-block sharded over the same ranks with the NCCL
+all-gather of key codes + V.  Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
 
@@ -55,6 +58,12 @@ def parse():
     ap.add_argument("--mode", default="forward", choices=["forward", "decode", "bwd"],
                     help="decode: SURVEY 8(f) N2, one new query row per sequence over a cached K/V of the config's n")
     ap.add_argument("--decode-batch", type=int, default=8, help="sequences per GPU in --mode decode")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong (default): the config's problem split by (batch, kv head) over the GPUs; weak: "
+                         "B = config B x GPUs, one batch element's heads per GPU group")
+    ap.add_argument("--seq-len", type=int, default=None, help="override n (e.g. --config long --seq-len 1048576)")
+    ap.add_argument("--no-long", action="store_true",
+                    help="skip the long_context block (128K tokens query-block sharded over the same GPUs)")
     ap.add_argument("--shard-seq", action="store_true",
                     help="query-block sharding of one sequence (default for --config long under torchrun, N>1; "
                          "with N=1 it exercises the same NCCL path on one GPU)")
@@ -189,7 +198,7 @@ def run_reference(args, W, rank):
     value = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(ts),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded counter-based generator, DESIGN.md input recipe)",
             "config": config_of(args, W),
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "oracle", "cpu_model": cpu_model(),
@@ -198,11 +207,18 @@ def run_reference(args, W, rank):
     print(json.dumps(line), flush=True)
 
 
-def config_of(args, W):
-    return {"workload": f"{args.config}: B={W.B} per GPU, H={W.H}, H_kv={W.H_kv}, n={W.n}, d={W.d}, d_v={W.d_v}, "
+def config_of(args, W, B_glob=None, world=1):
+    B_glob = W.B if B_glob is None else B_glob
+    units = B_glob * W.H_kv
+    par = (f"(batch, kv head) sharding (SURVEY 8(e)-1, sfa_dist_head_shard): the {units} units of the "
+           f"B={B_glob} problem in {world} contiguous range{'s' if world > 1 else ''}, "
+           f"{units // world}{'-' + str(-(-units // world)) if units % world else ''} per GPU; "
+           "no data-path collective")
+    return {"workload": f"{args.config}: B={B_glob}, H={W.H}, H_kv={W.H_kv}, n={W.n}, d={W.d}, d_v={W.d_v}, "
                         f"k={W.k}, {'causal' if W.causal else 'non-causal'}, {W.dtype} V",
-            "global_batch": W.B * args.gpus, "seq_len": W.n, "parallelism": f"weak: batch element r on rank r "
-            f"({args.gpus} GPU{'s' if args.gpus > 1 else ''}), no data-path collective",
+            "global_batch": B_glob, "seq_len": W.n,
+            "parallelism": par + (" (weak: B grows with the GPU count)" if getattr(args, "scaling", "strong") == "weak"
+                                  else " (strong: fixed global problem)"),
             "kernel": args.kernel,
             "semantics": ("R2 edges-only (A1/R2)" if getattr(args, "edges_only", False) else "R1 (A1)")
                          + (f", causal sliding window {args.window} (N4)" if getattr(args, "window", 0) else ""),
@@ -403,9 +419,11 @@ def run_decode(args, W, rank, world, local):
         print(json.dumps(line), flush=True)
 
 
-def run_sharded(args, W, rank, world, local):
+def measure_sharded(W, seed, rank, world, local, steps, warmup, workload_name="long"):
     """Long-context query-block sharding: one sequence of n tokens over `world`
-    GPUs, zig-zag chunks, one NCCL all-gather of key codes + V per step (strong scaling)."""
+    GPUs, zig-zag chunks (the library's sfa_dist_zigzag_chunk), one NCCL all-gather of key codes + V
+    per step through sfa_dist_allgather_kv (strong scaling).  Needs an initialised process group (for
+    the NCCL id broadcast).  Returns rank 0's JSON object (None elsewhere)."""
     import ctypes
 
     import torch
@@ -417,7 +435,6 @@ def run_sharded(args, W, rank, world, local):
     B, H, H_kv, n, d, d_v, k = W.B, W.H, W.H_kv, W.n, W.d, W.d_v, W.k
     c = sdist.chunk_size(n, world)
     chunks = sdist.owned_chunks(rank, world)
-    seed = accounting.SEEDS[args.config]
     bf = torch.bfloat16
 
     def local_fill(hh, dd, tid):  # chunk-major [2][B][hh][c][dd] slice of the global [B][hh][n][dd] tensor
@@ -468,15 +485,15 @@ def run_sharded(args, W, rank, world, local):
         if any(r):
             raise RuntimeError(f"sfa call failed: {r}")
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         flush.zero_()
         step()
     torch.cuda.synchronize()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(steps)]
     dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        for i in range(args.steps):
+        for i in range(steps):
             flush.zero_()
             step(evs[i])
         torch.cuda.synchronize()
@@ -484,36 +501,70 @@ def run_sharded(args, W, rank, world, local):
     per = [[e[j].elapsed_time(e[j + 1]) for j in range(4)] for e in evs]
     tot = torch.tensor([sum(sum(p) for p in per)], dtype=torch.float64, device=dev)
     dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    ms = float(tot.item()) / args.steps
-    stage = [sum(p[j] for p in per) / args.steps for j in range(4)]
-    attn_ms = torch.tensor([stage[3]], dtype=torch.float64, device=dev)
-    dist.all_reduce(attn_ms, op=dist.ReduceOp.MAX)
+    ms = float(tot.item()) / steps
+    stage = [sum(p[j] for p in per) / steps for j in range(4)]
+    stage_max = torch.tensor(stage, dtype=torch.float64, device=dev)
+    dist.all_reduce(stage_max, op=dist.ReduceOp.MAX)
+    stage_max = [float(x) for x in stage_max.tolist()]
     pairs_rank = B * H * sdist.causal_pairs_of_rank(rank, world, n)
     pk = peaks()
     mufu_peak = N_SMS * MUFU_EX2_PER_CLK_SM * pk["sm_max_mhz"] * 1e6
-    achieved = pairs_rank / (float(attn_ms.item()) / 1e3)
+    achieved = pairs_rank / (stage_max[3] / 1e3)
     ag_bytes = world * (ki.numel() + kv.numel() * 2 + V.numel() * 2)
     sh.close()
-    if rank == 0:
-        line = {"metric": METRIC, "value": B * n / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-                "data": "synthetic (seeded counter-based generator on device, DESIGN.md input recipe)",
-                "config": {"workload": f"long: B={B}, H={H}, H_kv={H_kv}, n={n}, d={d}, d_v={d_v}, k={k}, causal, "
-                                       f"bf16 V; one sequence sharded over {world} GPUs",
-                           "global_batch": B, "seq_len": n,
-                           "parallelism": f"zig-zag query blocks x{world} (chunks p, 2P-1-p of {c} tokens), "
-                                          "one NCCL all-gather of key codes + V per step",
-                           "l2": f"explicit {L2_FLUSH_MB} MB write between timed steps"},
-                "stage_ms": {"topk_qk": stage[0], "allgather_kv": stage[1], "prepare": stage[2], "attn": stage[3]},
-                "allgather_bytes_per_rank": ag_bytes,
-                "roofline": {"bound": "alu", "kernel": ("attn_sm100_ot_kernel" if W.d_v == 128 else "attn_sm100_kernel") + " (steps 4-8), per rank",
-                             "achieved": achieved / 1e9, "peak": mufu_peak / 1e9,
-                             "unit": "G pairs/s (1 MUFU ex2 per allowed causal pair)", "frac": achieved / mufu_peak,
-                             "traffic": None, "peak_source": "148 SMs x 16 ex2/clk x max SM clock"},
-                "cpu_baseline": None, "e2e": None,
-                "gpu_launches": 9 * args.steps, "clocks": clk.summary()}
-        print(json.dumps(line), flush=True)
+    if rank != 0:
+        return None
+    return {"metric": METRIC, "value": B * n / (ms / 1e3), "unit": "tokens/s", "n_gpus": world,
+            "steps": steps, "warmup": warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded counter-based generator on device, DESIGN.md input recipe)",
+            "config": {"workload": f"{workload_name}: B={B}, H={H}, H_kv={H_kv}, n={n}, d={d}, d_v={d_v}, k={k}, "
+                                   f"causal, bf16 V; one sequence query-block sharded over {world} GPU(s)",
+                       "global_batch": B, "seq_len": n,
+                       "parallelism": f"zig-zag query blocks x{world} (chunks p, 2P-1-p of {c} tokens), "
+                                      "one NCCL all-gather of key codes + V per step (sfa_dist_allgather_kv)",
+                       "l2": f"explicit {L2_FLUSH_MB} MB write between timed steps"},
+            "stage_ms": {"topk_qk": stage_max[0], "allgather_kv": stage_max[1], "prepare": stage_max[2],
+                         "attn": stage_max[3], "note": "each stage's max over ranks"},
+            "allgather_bytes_total": ag_bytes,
+            "allgather_bytes_received_per_rank": ag_bytes * (world - 1) // world,
+            "roofline": {"bound": "alu", "kernel": ("attn_sm100_ot_kernel" if W.d_v == 128 else "attn_sm100_kernel")
+                         + " (steps 4-8), slowest rank", "achieved": achieved / 1e9, "peak": mufu_peak / 1e9,
+                         "unit": "G pairs/s (1 MUFU ex2 per allowed causal pair)", "frac": achieved / mufu_peak,
+                         "traffic": None, "peak_source": "148 SMs x 16 ex2/clk x max SM clock"},
+            "cpu_baseline": None, "e2e": None,
+            "gpu_launches": 10 * steps, "clocks": clk.summary()}
+
+
+def spawn_ranks(args):
+    """`--gpus N` (N > 1) without a launcher: run this same command as N ranks under
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1) and exit with its status."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.run(cmd).returncode)
+
+
+def init_group(world, rank, local):
+    """torch.distributed for the plumbing: NCCL when there are several ranks; a 1-rank gloo group when a
+    single process needs a group (the NCCL id broadcast of the sharded path)."""
+    import torch
+    import torch.distributed as dist
+    if dist.is_initialized():
+        return
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    os.environ["MASTER_ADDR"], os.environ["MASTER_PORT"] = "127.0.0.1", str(s.getsockname()[1])
+    s.close()
+    dist.init_process_group("gloo", rank=0, world_size=1)
 
 
 def main():
@@ -521,58 +572,73 @@ def main():
     W = accounting.CONFIGS[args.config]
     if args.k is not None:
         W = accounting.Workload(**{**W.__dict__, "k": args.k})
+    if args.seq_len is not None:
+        W = accounting.Workload(**{**W.__dict__, "n": args.seq_len})
+    if args.impl == "reference":
+        run_reference(args, W, int(os.environ.get("RANK", "0")))
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        run_reference(args, W, rank)
-        return
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but this launch has WORLD_SIZE={world} ranks")
     import torch
     import torch.distributed as dist
 
+    from paper_2603_22300_b200 import dist as sdist
     from paper_2603_22300_b200 import inputs, sfa
     torch.cuda.set_device(local)
+    if torch.cuda.device_count() < world and local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} has no GPU (only {torch.cuda.device_count()} visible)")
     if args.mode == "bwd":
-        if world > 1 and not dist.is_initialized():
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if world > 1:
+            init_group(world, rank, local)
         run_bwd(args, W, rank, world, local)
         if world > 1:
             dist.destroy_process_group()
         return
     if args.mode == "decode":
-        if world > 1 and not dist.is_initialized():
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if world > 1:
+            init_group(world, rank, local)
         run_decode(args, W, rank, world, local)
         if world > 1:
             dist.destroy_process_group()
         return
     if args.shard_seq or (args.config == "long" and world > 1):
-        if not dist.is_initialized():
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("MASTER_PORT", "29533")
-            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
-        run_sharded(args, W, rank, world, local)
+        init_group(world, rank, local)
+        line = measure_sharded(W, accounting.SEEDS[args.config], rank, world, local, args.steps, args.warmup,
+                               workload_name=args.config)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
         dist.destroy_process_group()
         return
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_group(world, rank, local)
     kernel = {"auto": sfa.KERNEL_AUTO, "simt": sfa.KERNEL_SIMT, "sm100": sfa.KERNEL_SM100,
               "pair": sfa.KERNEL_SM100_PAIR, "wide": sfa.KERNEL_SM100_WIDE,
               "ot": sfa.KERNEL_SM100_OT}[args.kernel]
     dt = torch.bfloat16 if W.dtype == "bf16" else torch.float32
     seed = accounting.SEEDS[args.config]
-    B, H, H_kv, n, d, d_v, k = W.B, W.H, W.H_kv, W.n, W.d, W.d_v, W.k
     dev = torch.device("cuda", local)
-    # rank r holds batch element r of the global B = world batch: offset into the generator stream
+    # The global problem: B = W.B (strong scaling, the default) or W.B * world (weak: one batch element per
+    # rank).  It is split by (batch, kv head) units over the ranks (sfa_dist_head_shard): this
+    # rank's units [u0, u0 + sub.B) are contiguous in every global tensor, so the rank generates exactly that
+    # slice of the seeded global Q, K, V (generator offset = first element of its units) and runs the whole hot
+    # path on it as the problem (B = #units, H = H/H_kv, H_kv = 1).  No data-path collective.
+    B_glob = W.B * (world if args.scaling == "weak" else 1)
+    full = sfa.make_desc(B=B_glob, H=W.H, H_kv=W.H_kv, d=W.d, k=W.k, d_v=W.d_v, n_q=W.n, n_kv=W.n, causal=W.causal,
+                         dtype=sfa.SFA_BF16 if W.dtype == "bf16" else sfa.SFA_F32, kernel=kernel,
+                         edges_only=args.edges_only, window=args.window)
+    desc, u0 = sdist.head_shard(full, world, rank)
+    B, H, H_kv, n, d, d_v, k = desc.B, desc.H, desc.H_kv, W.n, W.d, W.d_v, W.k
     Q = torch.empty((B, H, n, d), dtype=dt, device=dev)
     K = torch.empty((B, H_kv, n, d), dtype=dt, device=dev)
     V = torch.empty((B, H_kv, n, d_v), dtype=dt, device=dev)
-    sfa.gen_fill(Q, seed, inputs.TID_Q, offset=rank * Q.numel())
-    sfa.gen_fill(K, seed, inputs.TID_K, offset=rank * K.numel())
-    sfa.gen_fill(V, seed, inputs.TID_V, offset=rank * V.numel())
-    desc = sfa.make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k, d_v=d_v, n_q=n, n_kv=n, causal=W.causal,
-                         dtype=sfa.SFA_BF16 if W.dtype == "bf16" else sfa.SFA_F32, kernel=kernel,
-                         edges_only=args.edges_only, window=args.window)
+    sfa.gen_fill(Q, seed, inputs.TID_Q, offset=u0 * H * n * d)
+    sfa.gen_fill(K, seed, inputs.TID_K, offset=u0 * n * d)
+    sfa.gen_fill(V, seed, inputs.TID_V, offset=u0 * n * d_v)
     q_idx = torch.empty((B, H, n, k), dtype=torch.uint8, device=dev)
     q_val = torch.empty((B, H, n, k), dtype=dt, device=dev)
     k_idx = torch.empty((B, H_kv, n, k), dtype=torch.uint8, device=dev)
@@ -661,12 +727,12 @@ def main():
         join_wait_ms = stage_ms[1] + stage_ms[2]
         stage_ms[1] = sum(kev[id(e)][0].elapsed_time(kev[id(e)][1]) for e in evs) / args.steps
         stage_ms[2] = sum(kev[id(e)][1].elapsed_time(kev[id(e)][2]) for e in evs) / args.steps
-    if world > 1:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    if world > 1:  # the whole-job step time is the slowest rank's; stages likewise
+        t = torch.tensor([tot_ms] + stage_ms, dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms = float(t.item())
+        tot_ms, stage_ms = float(t[0].item()), [float(x) for x in t[1:].tolist()]
     ms_per_step = tot_ms / args.steps
-    tokens_per_step = B * n * world
+    tokens_per_step = B_glob * n  # every rank's units together = the global problem
     value = tokens_per_step / (ms_per_step / 1e3)
     torch.cuda.synchronize()
     if int(status.item()) != 0:
@@ -734,9 +800,9 @@ def main():
 
     pk = peaks()
     attn_ms = stage_ms[3]
-    pairs = B * H * accounting.causal_pairs(n, n, 0, W.causal, args.window)
+    pairs = B * H * accounting.causal_pairs(n, n, 0, W.causal, args.window)  # this rank's units
     mufu_peak = N_SMS * MUFU_EX2_PER_CLK_SM * pk["sm_max_mhz"] * 1e6  # ex2/s
-    achieved = pairs / (attn_ms / 1e3)
+    achieved = pairs / (attn_ms / 1e3)  # attn_ms: the slowest rank's (ranks hold equal work up to one unit)
     traffic = None  # dram__bytes_read + dram__bytes_write per launch of the attention kernel (ncu --set full)
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -745,9 +811,20 @@ def main():
             traffic = ent["dram_bytes_per_launch"] if ent else None
         except Exception:
             traffic = None
-    topk_bytes = W.topk_bytes()
+    s_v = 2 if W.dtype == "bf16" else 4
+    topk_bytes = B * (H + H_kv) * n * (d * s_v + k * (1 + s_v))  # this rank's rows (stage times are its own)
     if fused_q:  # only the K rows go through the stand-alone top-k kernel
-        topk_bytes = B * H_kv * n * (d * 2 + k * 3)
+        topk_bytes = B * H_kv * n * (d * s_v + k * (1 + s_v))
+    # exact score interactions E of the whole job (prefix counts over the codes this step computed)
+    E_rank = accounting.exact_edges(q_idx, k_idx, d, causal=bool(W.causal)) if not args.window else None
+    E_total = None
+    if E_rank is not None:
+        E_total = E_rank
+        if world > 1:
+            t = torch.tensor([E_rank], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+            E_total = int(t.item())
+    pairs_total = B_glob * W.H * accounting.causal_pairs(n, n, 0, W.causal, args.window)
     sm100 = W.dtype == "bf16" and args.kernel != "simt"
     kname = {"auto": "attn_sm100_ot_kernel" if d_v == 128 else "attn_sm100_kernel", "sm100": "attn_sm100_kernel",
              "ot": "attn_sm100_ot_kernel", "pair": "attn_sm100_pair_kernel", "wide": "attn_sm100_wide_kernel",
@@ -778,25 +855,49 @@ def main():
         cpu = {"value": r["tokens_per_s"], "unit": "tokens/s", "cores": threads, "kind": "oracle",
                "cpu_model": cpu_model(),
                "sample": r["sample"], "sample_seconds": r["t_sample"]}
+    # the north star's long-context requirement in the same line: one 128K-token sequence query-block sharded
+    # over the same ranks (zig-zag + the NCCL all-gather of key codes and V), strong scaling
+    long_ctx = None
+    if not args.no_long and args.config != "long" and W.dtype == "bf16" and W.d_v == 128 and not args.window \
+            and not args.edges_only and args.kernel in ("auto", "ot"):
+        init_group(world, rank, local)
+        del flush
+        torch.cuda.empty_cache()
+        WL = accounting.CONFIGS["long"]
+        try:
+            long_ctx = measure_sharded(WL, accounting.SEEDS["long"], rank, world, local,
+                                       steps=max(2, min(args.steps, 5)), warmup=3)
+        except Exception as ex:  # reported, never hidden
+            long_ctx = {"error": str(ex)[:300]}
+        if long_ctx is not None:
+            long_ctx = {key: long_ctx[key] for key in ("value", "unit", "ms_per_step", "steps", "warmup", "scaling",
+                                                       "config", "stage_ms", "allgather_bytes_total",
+                                                       "allgather_bytes_received_per_rank", "roofline", "clocks")
+                        if key in long_ctx} if "error" not in long_ctx else long_ctx
     if rank == 0:
+        scaling = "weak" if args.scaling == "weak" else "strong"
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": W.dtype,
                 "data": "synthetic (seeded counter-based generator on device, DESIGN.md input recipe)",
-                "config": config_of(args, W),
+                "config": config_of(args, W, B_glob, world),
                 "stage_ms": {"topk_q": stage_ms[0], "topk_k": stage_ms[1], "prepare": stage_ms[2],
                              "attn": stage_ms[3],
                              "note": ("topk_k and prepare run on a second stream concurrently with topk_q; the step "
                                       f"waited {join_wait_ms:.4f} ms for them after topk_q")
-                             if join_wait_ms is not None else "stages back to back on one stream"},
-                "interactions_per_s": W.expected_interactions * pairs / (B * H * accounting.causal_pairs(n, n, 0, W.causal))
-                                      / (ms_per_step / 1e3) * world,
-                "pairs_per_s": pairs * world / (ms_per_step / 1e3),
+                             if join_wait_ms is not None else "stages back to back on one stream; each stage's "
+                                                              "max over ranks"},
+                "interactions": E_total,
+                "interactions_per_s": E_total / (ms_per_step / 1e3) if E_total is not None else None,
+                "interactions_note": "exact E = sum over allowed pairs of |S_i & S_j| (P:L114-120), prefix counts "
+                                     "over this step's codes (accounting.exact_edges)",
+                "pairs_per_s": pairs_total / (ms_per_step / 1e3),
                 "wall_s_timed_region": t_wall,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": (5 + int(args.edges_only) - int(fused_q) if sm100 else 4) * args.steps,
-                "clocks": clk.summary(), "context": context}
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": (5 + int(args.edges_only) - int(fused_q) if sm100 else 4) * args.steps,
+                "clocks": clk.summary(), "context": context, "long_context": long_ctx}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

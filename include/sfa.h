@@ -265,6 +265,34 @@ SFA_API sfa_status sfa_dist_allgather_kv(sfa_dist_t h, const sfa_attn_desc *loca
 SFA_API sfa_status sfa_dist_unpack_zigzag(const void *in, void *out, int32_t world, int64_t bh, int64_t chunk,
                                           int64_t row_bytes, sfa_stream_t stream);
 
+/* Host-only partition plans (no device, no NCCL; the CPU multi-process tests call them too):
+ *   sfa_dist_kv_plan    -- what sfa_dist_allgather_kv does for local_desc at `world` ranks: the three
+ *                          gathered tensors t = 0 (k_idx), 1 (k_val), 2 (V) each send bytes_per_rank[t]
+ *                          bytes per rank into staging at staging_offset[t] (rank-major), then are
+ *                          unpacked with sfa_dist_unpack_zigzag(world, bh, chunk, row_bytes[t]);
+ *                          staging_bytes = sfa_dist_staging_bytes.  Invalid desc -> INVALID_ARGUMENT.
+ *   sfa_dist_zigzag_chunk -- the zig-zag partition of n tokens: chunk length c = n/(2P)
+ *                          and the start q_pos0 of rank's chunk half (0: chunk rank, 1: chunk 2P-1-rank).
+ *                          n must be a positive multiple of 2P.
+ *   sfa_dist_head_shard -- the (batch, kv head) partition (no communication): the B*H_kv
+ *                          units of `full` (contiguous in every tensor: unit u = b*H_kv + g holds query heads
+ *                          [g*R, g*R+R), R = H/H_kv) split into `world` contiguous ranges whose sizes differ
+ *                          by at most one.  Rank `rank` gets units [unit0, unit0 + sub->B): *sub is the same
+ *                          problem with B = that count, H = R, H_kv = 1, so its tensors start at unit0 times
+ *                          the per-unit size of each tensor.  Fewer units than ranks -> UNSUPPORTED. */
+typedef struct {
+    int64_t bh, chunk;            /* (batch, kv head) rows and chunk length of the local desc            */
+    int64_t row_bytes[3];         /* bytes of one row of k_idx, k_val, V                                  */
+    int64_t bytes_per_rank[3];    /* bytes each rank contributes to each gather                           */
+    int64_t staging_offset[3];    /* 256-aligned offsets of the three rank-major blocks in the staging    */
+    int64_t staging_bytes;
+} sfa_dist_kv_plan_t;
+SFA_API sfa_status sfa_dist_kv_plan(const sfa_attn_desc *local_desc, int32_t world, sfa_dist_kv_plan_t *plan);
+SFA_API sfa_status sfa_dist_zigzag_chunk(int64_t n, int32_t world, int32_t rank, int32_t half, int64_t *chunk_len,
+                                         int64_t *q_pos0);
+SFA_API sfa_status sfa_dist_head_shard(const sfa_attn_desc *full, int32_t world, int32_t rank, sfa_attn_desc *sub,
+                                       int64_t *unit0);
+
 /* Build / device info: 1 if the calling thread's current device is sm_100 and the kernels load. */
 SFA_API int32_t sfa_device_supported(void);
 

@@ -94,3 +94,30 @@ CONFIGS = {
     "sweep": Workload(B=1, H=32, H_kv=8, n=16384, d=128, d_v=128, k=16),
 }
 SEEDS = {"tiny": 1, "gpt2": 11, "qwen3": 21, "long": 31, "sweep": 41}
+
+
+def exact_edges(q_idx, k_idx, d: int, q_pos0: int = 0, causal: bool = True) -> int:
+    """The exact number of score interactions E = sum over allowed pairs (i, j) of |S_i & S_j|
+    (P:L59), by one-hot prefix counts in O(n d) per (batch, kv head) instead of O(n^2 k):
+    E = sum_i sum_{u in S_i} #{allowed j : u in S_j}.  q_idx [B,H,n_q,k], k_idx [B,H_kv,n_kv,k] uint8
+    torch tensors on any device (the bench counts the codes it just computed, outside the timed region).
+    Supports are index sets (zero-valued selected entries count, reading A8)."""
+    import torch
+    B, H, n_q, _ = q_idx.shape
+    H_kv, n_kv = k_idx.shape[1], k_idx.shape[2]
+    R = H // H_kv
+    dev = q_idx.device
+    total = 0
+    last = torch.arange(n_q, device=dev, dtype=torch.int64) + q_pos0
+    for b in range(B):
+        for g in range(H_kv):
+            onehot = torch.zeros((n_kv, d), dtype=torch.int32, device=dev)
+            onehot.scatter_(1, k_idx[b, g].long(), 1)
+            pref = onehot.cumsum(0, dtype=torch.int64) if causal else onehot.sum(0, keepdim=True).expand(n_kv, d)
+            allowed = last.clamp(max=n_kv - 1) if causal else torch.full_like(last, n_kv - 1)
+            ok = (allowed >= 0)
+            rows = pref[allowed.clamp(min=0)]  # [n_q, d]: keys j <= allowed_i selecting each feature
+            for r in range(R):
+                cnt = rows.gather(1, q_idx[b, g * R + r].long()).sum(1)
+                total += int(torch.where(ok, cnt, torch.zeros_like(cnt)).sum().item())
+    return total

@@ -5,12 +5,13 @@
 Every ``csrc/*.cu`` is compiled with nvcc (``-gencode arch=compute_100a,code=sm_100a -lineinfo
 -O3``) into ``build/`` in parallel and linked into one shared library next to this file.
 Incremental: a source is recompiled when it, or any ``csrc/*.cuh`` / ``include/*.h``, is newer
-than its object.
+than its object; everything is rebuilt when the flags (incl. ``SFA_NVCC_FLAGS``) change.
 """
 from __future__ import annotations
 
 import concurrent.futures as cf
 import glob
+import hashlib
 import os
 import shutil
 import subprocess
@@ -43,8 +44,19 @@ def _deps_mtime() -> float:
     return max((os.path.getmtime(p) for p in deps), default=0.0)
 
 
+def _flags_stamp() -> str:
+    """The compile configuration the objects in build/ were made with: a change of ARCH, FLAGS or
+    SFA_NVCC_FLAGS (e.g. a -DSFA_WATCHDOG or -DSFA_MBAR_SUSPEND_NS=0 debug build) forces a full rebuild,
+    so tests and the bench never link objects of another configuration."""
+    return hashlib.sha256(" ".join(ARCH + FLAGS + extra_flags() + [nvcc()]).encode()).hexdigest()
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    stamp_path = os.path.join(BUILD, "flags.sha256")
+    stamp = _flags_stamp()
+    if not os.path.exists(stamp_path) or open(stamp_path).read().strip() != stamp:
+        force = True
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     dep_t = _deps_mtime()
     objs, jobs = [], []
@@ -67,6 +79,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         tmp = LIB + f".tmp{os.getpid()}"
         subprocess.check_call([nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-ldl"])
         os.replace(tmp, LIB)
+    with open(stamp_path, "w") as f:
+        f.write(stamp + "\n")
     return LIB
 
 

@@ -18,6 +18,8 @@ sfa_status from_cuda(cudaError_t e) { return e == cudaSuccess ? SFA_OK : SFA_ERR
 
 int key_tile(int k) { return k <= 32 ? 128 : 64; }
 
+int resolve_kernel(const sfa_attn_desc *d);
+
 sfa_status validate_desc(const sfa_attn_desc *d) {
     if (!d) return SFA_ERR_INVALID_ARGUMENT;
     if (d->B < 1 || d->H < 1 || d->H_kv < 1 || d->H % d->H_kv) return SFA_ERR_INVALID_ARGUMENT;
@@ -46,6 +48,11 @@ sfa_status validate_desc(const sfa_attn_desc *d) {
     if (d->edges_only && d->kernel != SFA_KERNEL_AUTO && d->kernel != SFA_KERNEL_SIMT &&
         d->kernel != SFA_KERNEL_SM100_OT)
         return SFA_ERR_UNSUPPORTED;  // R2 is built into the OT and SIMT kernels only
+    // grid.y limits, checked before any launch: the SIMT kernel puts B*H on grid.y, the R2 bitset
+    // kernel (edges.cu) B*H_kv (the V prep strides heads over grid.y and has no limit)
+    const int kern = resolve_kernel(d);
+    if (kern == SFA_KERNEL_SIMT && (int64_t)d->B * d->H > 65535) return SFA_ERR_UNSUPPORTED;
+    if (d->edges_only && kern == SFA_KERNEL_SM100_OT && (int64_t)d->B * d->H_kv > 65535) return SFA_ERR_UNSUPPORTED;
     return SFA_OK;
 }
 

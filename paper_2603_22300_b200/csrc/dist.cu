@@ -135,14 +135,61 @@ sfa_status sfa_dist_destroy(sfa_dist_t h) {
     return r == ncclSuccess ? SFA_OK : SFA_ERR_CUDA;
 }
 
-size_t sfa_dist_staging_bytes(const sfa_attn_desc *local_desc, int32_t world) {
+sfa_status sfa_dist_kv_plan(const sfa_attn_desc *local_desc, int32_t world, sfa_dist_kv_plan_t *plan) {
     const sfa_attn_desc *d = local_desc;
-    if (!d || world < 1 || d->B < 1 || d->H_kv < 1 || d->n_kv < 2 || (d->n_kv & 1) || d->k < 1 || d->d_v < 1)
-        return 0;
-    if (d->dtype != SFA_F32 && d->dtype != SFA_BF16) return 0;
-    const size_t rows = (size_t)world * d->B * d->H_kv * d->n_kv;
+    if (!d || !plan || world < 1 || d->B < 1 || d->H_kv < 1 || d->n_kv < 2 || (d->n_kv & 1) || d->k < 1 ||
+        d->d_v < 1)
+        return SFA_ERR_INVALID_ARGUMENT;
+    if (d->dtype != SFA_F32 && d->dtype != SFA_BF16) return SFA_ERR_INVALID_ARGUMENT;
+    const size_t es = esize(d->dtype);
+    const size_t rows_local = (size_t)d->B * d->H_kv * d->n_kv;
     auto al = [](size_t x) { return (x + 255) / 256 * 256; };
-    return al(rows * d->k) + al(rows * d->k * esize(d->dtype)) + al(rows * d->d_v * esize(d->dtype));
+    plan->bh = (int64_t)d->B * d->H_kv;
+    plan->chunk = d->n_kv / 2;
+    plan->row_bytes[0] = d->k;                   // k_idx rows (u8)
+    plan->row_bytes[1] = (int64_t)d->k * es;     // k_val rows
+    plan->row_bytes[2] = (int64_t)d->d_v * es;   // V rows
+    size_t off = 0;
+    for (int t = 0; t < 3; ++t) {
+        plan->bytes_per_rank[t] = (int64_t)(rows_local * plan->row_bytes[t]);
+        plan->staging_offset[t] = (int64_t)off;
+        off += al((size_t)plan->bytes_per_rank[t] * world);
+    }
+    plan->staging_bytes = (int64_t)off;
+    return SFA_OK;
+}
+
+size_t sfa_dist_staging_bytes(const sfa_attn_desc *local_desc, int32_t world) {
+    sfa_dist_kv_plan_t pl;
+    return sfa_dist_kv_plan(local_desc, world, &pl) == SFA_OK ? (size_t)pl.staging_bytes : 0;
+}
+
+sfa_status sfa_dist_zigzag_chunk(int64_t n, int32_t world, int32_t rank, int32_t half, int64_t *chunk_len,
+                                 int64_t *q_pos0) {
+    if (world < 1 || rank < 0 || rank >= world || (half != 0 && half != 1) || n < 2 * (int64_t)world ||
+        n % (2 * (int64_t)world))
+        return SFA_ERR_INVALID_ARGUMENT;
+    const int64_t c = n / (2 * (int64_t)world);
+    const int64_t q = half ? 2 * (int64_t)world - 1 - rank : rank;
+    if (chunk_len) *chunk_len = c;
+    if (q_pos0) *q_pos0 = q * c;
+    return SFA_OK;
+}
+
+sfa_status sfa_dist_head_shard(const sfa_attn_desc *full, int32_t world, int32_t rank, sfa_attn_desc *sub,
+                               int64_t *unit0) {
+    if (!full || !sub || !unit0 || world < 1 || rank < 0 || rank >= world) return SFA_ERR_INVALID_ARGUMENT;
+    if (full->B < 1 || full->H < 1 || full->H_kv < 1 || full->H % full->H_kv) return SFA_ERR_INVALID_ARGUMENT;
+    const int64_t units = (int64_t)full->B * full->H_kv;
+    if (units < world) return SFA_ERR_UNSUPPORTED;  // a rank would get no (batch, kv head) unit
+    const int64_t u0 = units * rank / world, u1 = units * (rank + 1) / world;
+    if (u1 - u0 > INT32_MAX) return SFA_ERR_UNSUPPORTED;
+    *sub = *full;
+    sub->B = (int32_t)(u1 - u0);  // each unit is its own batch element of H/H_kv query heads, 1 kv head
+    sub->H = full->H / full->H_kv;
+    sub->H_kv = 1;
+    *unit0 = u0;
+    return SFA_OK;
 }
 
 sfa_status sfa_dist_unpack_zigzag(const void *in, void *out, int32_t world, int64_t bh, int64_t chunk,
@@ -159,31 +206,34 @@ sfa_status sfa_dist_allgather_kv(sfa_dist_t h, const sfa_attn_desc *local_desc, 
                                  const void *k_val_local, const void *v_local, uint8_t *k_idx_full, void *k_val_full,
                                  void *v_full, void *staging, size_t staging_bytes, sfa_stream_t stream) {
     if (!h || !local_desc) return SFA_ERR_INVALID_ARGUMENT;
-    const sfa_attn_desc *d = local_desc;
-    const size_t need = sfa_dist_staging_bytes(d, h->world);
-    if (need == 0) return SFA_ERR_INVALID_ARGUMENT;
+    sfa_dist_kv_plan_t pl;
+    if (sfa_dist_kv_plan(local_desc, h->world, &pl) != SFA_OK) return SFA_ERR_INVALID_ARGUMENT;
+    const size_t need = (size_t)pl.staging_bytes;
     if (!k_idx_local || !k_val_local || !v_local || !k_idx_full || !k_val_full || !v_full || !staging)
+        return SFA_ERR_INVALID_ARGUMENT;
+    // every tensor 16-byte aligned (include/sfa.h conventions): the unpack moves 16-byte words when a
+    // row is a multiple of 16 bytes, so a misaligned buffer must be rejected here, before any launch
+    if ((((uintptr_t)k_idx_local) | ((uintptr_t)k_val_local) | ((uintptr_t)v_local) | ((uintptr_t)k_idx_full) |
+         ((uintptr_t)k_val_full) | ((uintptr_t)v_full) | ((uintptr_t)staging)) & 15u)
         return SFA_ERR_INVALID_ARGUMENT;
     if (staging_bytes < need) return SFA_ERR_RESOURCE;
     const NcclApi &api = nccl();
     cudaStream_t st = (cudaStream_t)stream;
     const int P = h->world;
-    const int64_t bh = (int64_t)d->B * d->H_kv, c = d->n_kv / 2;
-    const size_t es = esize(d->dtype);
-    const size_t rows_local = (size_t)bh * d->n_kv;
-    const size_t b_idx = rows_local * d->k, b_val = rows_local * d->k * es, b_v = rows_local * d->d_v * es;
-    auto al = [](size_t x) { return (x + 255) / 256 * 256; };
-    uint8_t *s_idx = (uint8_t *)staging;
-    uint8_t *s_val = s_idx + al(b_idx * P);
-    uint8_t *s_v = s_val + al(b_val * P);
+    // one grouped all-gather of the three rank-major blocks, then the unpack into sequence order; the
+    // offsets and sizes come from sfa_dist_kv_plan (also what the CPU multi-process tests execute)
+    const void *src[3] = {k_idx_local, k_val_local, v_local};
+    void *dst[3] = {k_idx_full, k_val_full, v_full};
     if (api.GroupStart() != ncclSuccess) return SFA_ERR_CUDA;
-    bool ok = api.AllGather(k_idx_local, s_idx, b_idx, ncclUint8, h->comm, st) == ncclSuccess;
-    ok = ok && api.AllGather(k_val_local, s_val, b_val, ncclUint8, h->comm, st) == ncclSuccess;
-    ok = ok && api.AllGather(v_local, s_v, b_v, ncclUint8, h->comm, st) == ncclSuccess;
+    bool ok = true;
+    for (int t = 0; t < 3; ++t)
+        ok = ok && api.AllGather(src[t], (uint8_t *)staging + pl.staging_offset[t], (size_t)pl.bytes_per_rank[t],
+                                 ncclUint8, h->comm, st) == ncclSuccess;
     if (api.GroupEnd() != ncclSuccess || !ok) return SFA_ERR_CUDA;
-    if (launch_unpack(s_idx, k_idx_full, P, bh, c, d->k, st) != cudaSuccess) return SFA_ERR_CUDA;
-    if (launch_unpack(s_val, k_val_full, P, bh, c, (int64_t)d->k * es, st) != cudaSuccess) return SFA_ERR_CUDA;
-    if (launch_unpack(s_v, v_full, P, bh, c, (int64_t)d->d_v * es, st) != cudaSuccess) return SFA_ERR_CUDA;
+    for (int t = 0; t < 3; ++t)
+        if (launch_unpack((uint8_t *)staging + pl.staging_offset[t], dst[t], P, pl.bh, pl.chunk, pl.row_bytes[t],
+                          st) != cudaSuccess)
+            return SFA_ERR_CUDA;
     return SFA_OK;
 }
 

@@ -43,10 +43,13 @@ cudaError_t launch_bucket(const uint8_t *k_idx, const void *k_val, bool bf16, in
 // P.V operand prep for the sm100 kernel: amax[bh] = max|V| bits, v16 = fp16(V * 2^-e) (vprep.cu)
 cudaError_t launch_vprep(const void *v, int64_t bh_kv, int64_t n_kv, int d_v, uint32_t *amax, void *v16,
                          cudaStream_t stream);
-// e >= 0 with max|V| * 2^-e < 2^15 (fp16-safe); shared by vprep.cu and the attention epilogue
+// e with max|V| * 2^-e in [2^14, 2^15) (fp16-safe and clear of fp16's subnormal range, in either
+// direction: small heads are scaled UP), clamped to e >= -126 so that 2^-e and 2^e are both normal
+// floats; e = 0 for an all-zero head.  Shared by vprep.cu and the attention epilogues.
 __device__ __forceinline__ int vprep_head_exp(uint32_t amax_bits) {
-    const int E = (int)((amax_bits >> 23) & 0xFF) - 127;
-    return E > 14 ? E - 14 : 0;
+    if (amax_bits == 0u) return 0;
+    const int e = (int)((amax_bits >> 23) & 0xFF) - 127 - 14;
+    return e < -126 ? -126 : e;
 }
 // decode shape (rows = n_q * H / H_kv <= 16 per kv head): split-KV CUDA-core kernel + LSE merge
 // (decode.cu); ws >= decode_workspace_bytes

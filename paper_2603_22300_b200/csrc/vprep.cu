@@ -3,8 +3,9 @@
 // The tensor-core P.V takes A = P and B = V in the same 16-bit format.  Rounding P to bf16 costs
 // 2^-9 relative per weight, which alone can exceed the 2e-3 bar on |O| ~ 1 rows; fp16 P costs
 // 2^-12.  V therefore goes to fp16 too, EXACTLY: V' = V * 2^-e with one power of two per
-// (batch, kv head) chosen so max|V'| < 2^15 (bf16's 8-bit significand fits fp16's 11 bits; only
-// |V'| < 2^-14, i.e. below 2^-29 max|V|, loses bits to fp16 subnormals).  The attention epilogue
+// (batch, kv head) chosen so max|V'| lies in [2^14, 2^15) -- scaled down for large heads and UP for
+// small ones (bf16's 8-bit significand fits fp16's 11 bits; only |V'| < 2^-14, i.e. below about
+// 2^-28 max|V| of the head, loses bits to fp16 subnormals).  The attention epilogue
 // multiplies O by 2^e.  Two HBM-bound passes: absmax per head, then convert.
 #include <cuda_fp16.h>
 
@@ -16,8 +17,8 @@ namespace {
 
 // absmax of |V| per (b, kv head): float bits of a non-negative value order like unsigned ints
 __global__ void __launch_bounds__(256) v_absmax_kernel(const uint4 *__restrict__ v, int64_t vec_per_head,
-                                                        uint32_t *__restrict__ amax) {
-    const int bh = blockIdx.y;
+                                                        int64_t n_bh, uint32_t *__restrict__ amax) {
+    for (int64_t bh = blockIdx.y; bh < n_bh; bh += gridDim.y) {  // grid.y <= 65535: heads strided
     const uint4 *src = v + (int64_t)bh * vec_per_head;
     uint32_t m = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < vec_per_head;
@@ -33,11 +34,13 @@ __global__ void __launch_bounds__(256) v_absmax_kernel(const uint4 *__restrict__
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) atomicMax(amax + bh, m);
+    }
 }
 
 __global__ void __launch_bounds__(256) v_to_f16_kernel(const uint4 *__restrict__ v, int64_t vec_per_head,
-                                                        const uint32_t *__restrict__ amax, uint2 *__restrict__ out) {
-    const int bh = blockIdx.y;
+                                                        int64_t n_bh, const uint32_t *__restrict__ amax,
+                                                        uint2 *__restrict__ out) {
+    for (int64_t bh = blockIdx.y; bh < n_bh; bh += gridDim.y) {
     const int e = vprep_head_exp(__ldg(amax + bh));
     const float sc = __uint_as_float((uint32_t)(127 - e) << 23);  // 2^-e, exact
     const uint4 *src = v + (int64_t)bh * vec_per_head;
@@ -53,6 +56,7 @@ __global__ void __launch_bounds__(256) v_to_f16_kernel(const uint4 *__restrict__
             o[q] = *reinterpret_cast<const uint32_t *>(&h);
         }
         dst[i] = make_uint4(o[0], o[1], o[2], o[3]);
+    }
     }
 }
 
@@ -71,9 +75,9 @@ cudaError_t launch_vprep(const void *v, int64_t bh_kv, int64_t n_kv, int d_v, ui
     const int64_t cap = ((int64_t)sms * 8 + bh_kv - 1) / bh_kv;  // about 8 CTAs per SM in total
     if (gx > cap) gx = cap;
     if (gx < 1) gx = 1;
-    dim3 grid((unsigned)gx, (unsigned)bh_kv);
-    v_absmax_kernel<<<grid, 256, 0, stream>>>((const uint4 *)v, vec, amax);
-    v_to_f16_kernel<<<grid, 256, 0, stream>>>((const uint4 *)v, vec, amax, (uint2 *)v16);
+    dim3 grid((unsigned)gx, (unsigned)(bh_kv < 65535 ? bh_kv : 65535));
+    v_absmax_kernel<<<grid, 256, 0, stream>>>((const uint4 *)v, vec, bh_kv, amax);
+    v_to_f16_kernel<<<grid, 256, 0, stream>>>((const uint4 *)v, vec, bh_kv, amax, (uint2 *)v16);
     return cudaGetLastError();
 }
 

@@ -29,6 +29,13 @@ class SfaError(RuntimeError):
         self.code = code
 
 
+class KvPlan(ctypes.Structure):
+    """sfa_dist_kv_plan_t (include/sfa.h)."""
+    _fields_ = [("bh", ctypes.c_int64), ("chunk", ctypes.c_int64), ("row_bytes", ctypes.c_int64 * 3),
+                ("bytes_per_rank", ctypes.c_int64 * 3), ("staging_offset", ctypes.c_int64 * 3),
+                ("staging_bytes", ctypes.c_int64)]
+
+
 class AttnDesc(ctypes.Structure):
     _fields_ = [("B", ctypes.c_int32), ("H", ctypes.c_int32), ("H_kv", ctypes.c_int32),
                 ("d", ctypes.c_int32), ("k", ctypes.c_int32), ("d_v", ctypes.c_int32),
@@ -74,6 +81,9 @@ def lib() -> ctypes.CDLL:
             "sfa_attn_bwd_workspace_bytes": ([D], SZ),
             "sfa_attn_bwd": ([D, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P], I32),
             "sfa_attn_fwd_fused_q": ([D, P, P, P, P, P, P, P, P, P, P, SZ, P], I32),
+            "sfa_dist_kv_plan": ([D, I32, ctypes.POINTER(KvPlan)], I32),
+            "sfa_dist_zigzag_chunk": ([I64, I32, I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I64)], I32),
+            "sfa_dist_head_shard": ([D, I32, I32, D, ctypes.POINTER(I64)], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -87,7 +97,8 @@ EXPORTS = ("sfa_status_string", "sfa_topk_codes", "sfa_attn_workspace_bytes", "s
            "sfa_forward_host", "sfa_device_supported", "sfa_gen_fill", "sfa_debug_sm100_scores",
            "sfa_attn_prepare", "sfa_attn_fwd_prepared", "sfa_dist_unique_id", "sfa_dist_init", "sfa_dist_destroy",
            "sfa_dist_staging_bytes", "sfa_dist_allgather_kv", "sfa_dist_unpack_zigzag", "sfa_forward_host_pipelined",
-           "sfa_attn_bwd_workspace_bytes", "sfa_attn_bwd", "sfa_attn_fwd_fused_q")
+           "sfa_attn_bwd_workspace_bytes", "sfa_attn_bwd", "sfa_attn_fwd_fused_q", "sfa_dist_kv_plan",
+           "sfa_dist_zigzag_chunk", "sfa_dist_head_shard")
 
 
 def _check(code: int, where: str):
@@ -115,6 +126,46 @@ def _dev(*ts):
     for t in ts:
         if not (t.is_cuda and t.is_contiguous()):
             raise ValueError("tensors must be contiguous CUDA tensors")
+
+
+def _expect(t, shape, dtype, name):
+    """The C ABI sees raw pointers only: every shape / dtype it relies on is checked here."""
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: dtype {t.dtype}, expected {dtype}")
+
+
+def _check_codes(q_idx, q_val, k_idx, k_val, v, d):
+    """Codes and V of one attention call: q [B,H,n_q,k], k [B,H_kv,n_kv,k], v [B,H_kv,n_kv,d_v]; the value
+    tensors share v's dtype (bf16 or fp32), indices are u8."""
+    _dt(v)
+    if q_idx.dim() != 4 or k_idx.dim() != 4 or v.dim() != 4:
+        raise ValueError("q_idx, k_idx and v must be 4-D ([B, heads, n, .])")
+    B, H, n_q, k = q_idx.shape
+    _, H_kv, n_kv, _ = k_idx.shape
+    if not 1 <= k <= d:
+        raise ValueError(f"code size k={k} must lie in [1, d={d}]")
+    _expect(q_idx, (B, H, n_q, k), torch.uint8, "q_idx")
+    _expect(q_val, (B, H, n_q, k), v.dtype, "q_val")
+    _expect(k_idx, (B, H_kv, n_kv, k), torch.uint8, "k_idx")
+    _expect(k_val, (B, H_kv, n_kv, k), v.dtype, "k_val")
+    _expect(v, (B, H_kv, n_kv, v.shape[-1]), v.dtype, "v")
+    if H_kv < 1 or H % H_kv:
+        raise ValueError(f"H={H} must be a multiple of H_kv={H_kv}")
+
+
+def _check_out(out, B, H, n_q, d_v, dtype):
+    o, lse = out
+    _dev(o, lse)
+    _expect(o, (B, H, n_q, d_v), dtype, "out[0] (O)")
+    _expect(lse, (B, H, n_q), torch.float32, "out[1] (LSE)")
+
+
+def _check_ws(ws, nbytes):
+    _dev(ws)
+    if ws.dtype != torch.uint8 or ws.numel() < nbytes:
+        raise ValueError(f"workspace must be a uint8 tensor of >= {nbytes} bytes")
 
 
 def make_desc(*, B, H, H_kv, d, k, d_v, n_q, n_kv, q_pos0=0, causal=True, scale=None, dtype=SFA_BF16,
@@ -159,11 +210,15 @@ def attn_fwd(q_idx, q_val, k_idx, k_val, v, *, d, causal=True, scale=None, q_pos
     """Stage 2: (O, LSE) = FlashSFA forward over the codes (bucketing + attention kernels).
     edges_only: reading A1/R2 -- only the pairs whose supports intersect enter the softmax."""
     _dev(q_idx, q_val, k_idx, k_val, v)
+    _check_codes(q_idx, q_val, k_idx, k_val, v, d)
     desc = _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, kernel, _dt(v), edges_only, window)
     B, H, n_q, _ = q_idx.shape
     nb = workspace_bytes(desc)
     if workspace is None:
         workspace = torch.empty(max(nb, 16), dtype=torch.uint8, device=v.device)
+    _check_ws(workspace, nb)
+    if out is not None:
+        _check_out(out, B, H, n_q, v.shape[-1], v.dtype)
     if out is None:
         o = torch.empty((B, H, n_q, v.shape[-1]), dtype=v.dtype, device=v.device)
         lse = torch.empty((B, H, n_q), dtype=torch.float32, device=v.device)
@@ -181,6 +236,11 @@ def attn_fwd_fused_q(q, k_idx, k_val, v, *, causal=True, scale=None, q_pos0=0, k
     _dev(q, k_idx, k_val, v)
     B, H, n_q, d = q.shape
     _, H_kv, n_kv, k = k_idx.shape
+    if q.dtype != torch.bfloat16 or v.dtype != torch.bfloat16:
+        raise TypeError("the fused path takes bf16 q and v")
+    _expect(k_val, (B, H_kv, n_kv, k), v.dtype, "k_val")
+    _expect(k_idx, (B, H_kv, n_kv, k), torch.uint8, "k_idx")
+    _expect(v, (B, H_kv, n_kv, v.shape[-1]), v.dtype, "v")
     desc = make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k, d_v=v.shape[-1], n_q=n_q, n_kv=n_kv, q_pos0=q_pos0,
                      causal=causal, scale=scale, dtype=_dt(v), kernel=kernel)
     ws = torch.empty(max(workspace_bytes(desc), 16), dtype=torch.uint8, device=v.device)
@@ -199,6 +259,8 @@ def bucket_keys(k_idx, k_val, *, d, n_q=1, H=None, d_v=64, causal=True, workspac
     """Step 3 alone: the key-tile feature buckets (uint8 workspace tensor)."""
     _dev(k_idx, k_val)
     B, H_kv, n_kv, k = k_idx.shape
+    _expect(k_val, (B, H_kv, n_kv, k), k_val.dtype, "k_val")
+    _dt(k_val)
     desc = make_desc(B=B, H=H or H_kv, H_kv=H_kv, d=d, k=k, d_v=d_v, n_q=n_q, n_kv=n_kv, causal=causal,
                      dtype=_dt(k_val), kernel=KERNEL_SIMT)  # buckets feed the CUDA-core kernel
     nb = workspace_bytes(desc)
@@ -211,6 +273,14 @@ def bucket_keys(k_idx, k_val, *, d, n_q=1, H=None, d_v=64, causal=True, workspac
 
 def attn_fwd_bucketed(desc: AttnDesc, q_idx, q_val, v, workspace, out=None):
     _dev(q_idx, q_val, v, workspace)
+    _expect(q_idx, (desc.B, desc.H, desc.n_q, desc.k), torch.uint8, "q_idx")
+    _expect(q_val, (desc.B, desc.H, desc.n_q, desc.k), v.dtype, "q_val")
+    _expect(v, (desc.B, desc.H_kv, desc.n_kv, desc.d_v), v.dtype, "v")
+    if _dt(v) != desc.dtype:
+        raise TypeError("v's dtype differs from the desc the buckets were built for")
+    _check_ws(workspace, workspace_bytes(desc))
+    if out is not None:
+        _check_out(out, desc.B, desc.H, desc.n_q, desc.d_v, v.dtype)
     if out is None:
         o = torch.empty((desc.B, desc.H, desc.n_q, desc.d_v), dtype=v.dtype, device=v.device)
         lse = torch.empty((desc.B, desc.H, desc.n_q), dtype=torch.float32, device=v.device)
@@ -225,6 +295,7 @@ def debug_sm100_scores(q_idx, q_val, k_idx, k_val, v, *, d, causal=True, scale=N
     """Diagnostic: run the sm_100a kernel and return (O, LSE, S) where S [128, 128] fp32 is the raw
     score tile Q~ K~^T of the first key tile of work item 0 / query tile 0 (include/sfa.h)."""
     _dev(q_idx, q_val, k_idx, k_val, v)
+    _check_codes(q_idx, q_val, k_idx, k_val, v, d)
     desc = _desc_from_codes(q_idx, k_idx, v, d, causal, scale, 0, kernel, _dt(v))
     B, H, n_q, _ = q_idx.shape
     o = torch.empty((B, H, n_q, v.shape[-1]), dtype=v.dtype, device=v.device)
@@ -244,12 +315,24 @@ def attn_bwd(q_idx, q_val, k_idx, k_val, v, o, lse, dO, *, d, causal=True, scale
     """Backward with the straight-through rule (include/sfa.h sfa_attn_bwd): returns fp32
     (dq_val [B,H,n_q,k], dk_val [B,H_kv,n_kv,k], dv [B,H_kv,n_kv,d_v])."""
     _dev(q_idx, q_val, k_idx, k_val, v, o, lse, dO)
+    _check_codes(q_idx, q_val, k_idx, k_val, v, d)
     desc = _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, KERNEL_AUTO, _dt(v))
     B, H, n_q, k = q_idx.shape
     _, H_kv, n_kv, _ = k_idx.shape
+    d_v = v.shape[-1]
+    if v.dtype != torch.bfloat16:
+        raise TypeError("the backward takes bf16 codes, v, o and dO")
+    _check_out((o, lse), B, H, n_q, d_v, v.dtype)
+    _expect(dO, (B, H, n_q, d_v), torch.bfloat16, "dO")
+    nb = int(lib().sfa_attn_bwd_workspace_bytes(ctypes.byref(desc)))
     if workspace is None:
-        workspace = torch.empty(max(int(lib().sfa_attn_bwd_workspace_bytes(ctypes.byref(desc))), 16),
-                                dtype=torch.uint8, device=v.device)
+        workspace = torch.empty(max(nb, 16), dtype=torch.uint8, device=v.device)
+    _check_ws(workspace, nb)
+    if out is not None:
+        _dev(*out)
+        _expect(out[0], (B, H, n_q, k), torch.float32, "dq_val")
+        _expect(out[1], (B, H_kv, n_kv, k), torch.float32, "dk_val")
+        _expect(out[2], (B, H_kv, n_kv, d_v), torch.float32, "dv")
     if out is None:
         f32 = dict(dtype=torch.float32, device=v.device)
         out = (torch.empty((B, H, n_q, k), **f32), torch.empty((B, H_kv, n_kv, k), **f32),
@@ -271,10 +354,18 @@ def forward(q, k, v, *, k_code, causal=True, scale=None, q_pos0=0, kernel=KERNEL
     _dev(q, k, v)
     B, H, n_q, d = q.shape
     _, H_kv, n_kv, _ = k.shape
+    _dt(v)
+    _expect(q, (B, H, n_q, d), v.dtype, "q")
+    _expect(k, (B, H_kv, n_kv, d), v.dtype, "k")
+    _expect(v, (B, H_kv, n_kv, v.shape[-1]), v.dtype, "v")
     desc = make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k_code, d_v=v.shape[-1], n_q=n_q, n_kv=n_kv, q_pos0=q_pos0,
                      causal=causal, scale=scale, dtype=_dt(v), kernel=kernel, edges_only=edges_only, window=window)
+    nb = scratch_bytes(desc)
     if scratch is None:
-        scratch = torch.empty(max(scratch_bytes(desc), 16), dtype=torch.uint8, device=v.device)
+        scratch = torch.empty(max(nb, 16), dtype=torch.uint8, device=v.device)
+    _check_ws(scratch, nb)
+    if out is not None:
+        _check_out(out, B, H, n_q, v.shape[-1], v.dtype)
     if out is None:
         o = torch.empty((B, H, n_q, v.shape[-1]), dtype=v.dtype, device=v.device)
         lse = torch.empty((B, H, n_q), dtype=torch.float32, device=v.device)

@@ -47,6 +47,20 @@ def o_as_f64(o, dtype):
     return (inputs.bf16_bits_to_f32(o) if dtype == "bf16" else o).astype(np.float64)
 
 
+def _log_parity(err_o, plain, err_l, n_el, n_small):
+    """SFA_PARITY_LOG=<file>: one JSON line per bf16 comparison (test id, errors) -- the committed parity
+    headroom summary (profiles/) is made from it."""
+    import json
+    import os
+    path = os.environ.get("SFA_PARITY_LOG")
+    if not path:
+        return
+    with open(path, "a") as f:
+        f.write(json.dumps({"test": os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0],
+                            "max_excess_o": float(err_o), "max_abs_o_small": plain, "max_abs_lse": float(err_l),
+                            "elements": int(n_el), "elements_abs_o_lt_0.5": n_small}) + "\n")
+
+
 def assert_attn_close(o_gpu, lse_gpu, o_ref, lse_ref, dtype):
     """o_gpu/lse_gpu: numpy (o in storage dtype); refs fp64."""
     og = o_as_f64(o_gpu, dtype)
@@ -62,7 +76,13 @@ def assert_attn_close(o_gpu, lse_gpu, o_ref, lse_ref, dtype):
         excess = np.abs(og - o_ref) - BF16_U * np.abs(o_ref)
         err_o = excess.max()
         err_l = np.abs(lg - lse_ref).max()
+        # the north star's plain max-abs bar where it applies outright (|O| < 0.5: the bf16 output rounding
+        # is <= 2^-10 there), so the headroom is visible
+        small = np.abs(o_ref) < 0.5
+        plain = float(np.abs(og - o_ref)[small].max()) if small.any() else 0.0
+        _log_parity(err_o, plain, err_l, og.size, int(small.sum()))
         assert err_o <= TOL_BF16, f"max (|dO| - 2^-8|O_ref|) = {err_o}"
+        assert plain <= TOL_BF16, f"max |dO| over |O_ref| < 0.5 = {plain}"
         assert err_l <= TOL_BF16, f"max |dLSE| = {err_l}"
     else:
         err_o = (np.abs(og - o_ref) / np.maximum(1.0, np.abs(o_ref))).max()
@@ -70,3 +90,14 @@ def assert_attn_close(o_gpu, lse_gpu, o_ref, lse_ref, dtype):
         assert err_o <= TOL_F32_REL, f"max rel |dO| = {err_o}"
         assert err_l <= TOL_F32_REL, f"max rel |dLSE| = {err_l}"
     return err_o, err_l
+
+
+def gen_big(seed, tensor_id, shape, dtype, chunk=1 << 24):
+    """inputs.gen for tensors too large to hash in one numpy call (256K-1M configs): the same values,
+    generated chunk by chunk of flat indices (bounded temporary memory)."""
+    total = int(np.prod(shape))
+    out = np.empty(total, np.uint16 if dtype == "bf16" else np.float32)
+    for s in range(0, total, chunk):
+        e = min(total, s + chunk)
+        out[s:e] = inputs.gen(seed, tensor_id, shape, dtype, flat=np.arange(s, e, dtype=np.int64))
+    return out.reshape(shape)

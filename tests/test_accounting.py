@@ -72,3 +72,17 @@ def test_appb_flop_table():
 def test_causal_pairs(n_q, n_kv, q_pos0):
     brute = sum(1 for i in range(n_q) for j in range(n_kv) if j <= q_pos0 + i)
     assert accounting.causal_pairs(n_q, n_kv, q_pos0) == brute
+
+
+@pytest.mark.parametrize("causal,q_pos0", [(True, 0), (False, 0), (True, 37)])
+def test_exact_edges_torch_prefix_count_equals_oracle(causal, q_pos0):
+    """The bench's exact interaction count (accounting.exact_edges, torch prefix counts) equals the
+    oracle's explicit pair-by-pair overlap count, GQA and skewed supports included."""
+    import torch
+    q, k, _ = inputs.qkv(5, 2, 4, 2, 80, 64, 8, "bf16", variant="skewed", n_kv=80 + q_pos0)
+    qi, _ = oracle.topk_codes(q.reshape(-1, 64), 8)
+    ki, _ = oracle.topk_codes(k.reshape(-1, 64), 8)
+    qi = qi.reshape(2, 4, 80, 8)
+    ki = ki.reshape(2, 2, 80 + q_pos0, 8)
+    E = accounting.exact_edges(torch.from_numpy(qi), torch.from_numpy(ki), 64, q_pos0=q_pos0, causal=causal)
+    assert E == oracle.edge_count(qi, ki, causal=causal, q_pos0=q_pos0)

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import oracle
-from helpers import assert_attn_close, from_torch, host_qkv, oracle_codes, to_torch
+from helpers import assert_attn_close, from_torch, gen_big, host_qkv, oracle_codes, to_torch
 from paper_2603_22300_b200 import inputs
 
 pytestmark = pytest.mark.gpu
@@ -209,8 +209,8 @@ def big_case(lib, seed, B, H, H_kv, n, d, d_v, k, kernel=0, per_head=16):
     # oracle inputs regenerated on the host: the sampled query rows, all keys and values
     qflat = (rows[:, None] * d + np.arange(d)[None, :])
     q_rows = inputs.gen(seed, inputs.TID_Q, (B, H, n, d), "bf16", flat=qflat)
-    kx = inputs.gen(seed, inputs.TID_K, (B, H_kv, n, d), "bf16")
-    v = inputs.gen(seed, inputs.TID_V, (B, H_kv, n, d_v), "bf16")
+    kx = gen_big(seed, inputs.TID_K, (B, H_kv, n, d), "bf16")
+    v = gen_big(seed, inputs.TID_V, (B, H_kv, n, d_v), "bf16")
     ki, kv = oracle_codes(kx, k)
     qi_r, qv_r = oracle_codes(q_rows, k)
     # scatter the sampled query codes into a full-size code tensor (other rows unused by the oracle)
@@ -238,6 +238,9 @@ def test_sweep_config_sampled(lib, k):
 
 
 @pytest.mark.slow
-def test_long_config_sampled(lib):
-    """BASELINE configs[3] at n=131072 on one GPU (the sharded runs must reproduce it)."""
-    big_case(lib, 31, 1, 32, 8, 131072, 128, 128, 16, per_head=2)
+@pytest.mark.parametrize("n", [131072, 262144, 524288, 1048576])
+def test_long_config_sampled(lib, n):
+    """BASELINE configs[3] ("n=128K-1M") on one GPU: the whole 1M-token problem (Q 8 GiB, O 8 GiB) fits
+    one B200; sampled rows incl. tile boundaries and the last rows against the oracle (the sharded runs
+    must reproduce these rows bit for bit)."""
+    big_case(lib, 31, 1, 32, 8, n, 128, 128, 16, per_head=2 if n <= 262144 else 1)

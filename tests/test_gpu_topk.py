@@ -86,3 +86,21 @@ def test_qwen3_shape_all_rows(lib):
     oi, ov = oracle_codes(k_host, 16)
     np.testing.assert_array_equal(from_torch(gi), oi)
     np.testing.assert_array_equal(from_torch(gv), ov)
+
+
+@pytest.mark.slow
+def test_qwen3_q_codes_all_rows(lib):
+    """Every row of a Qwen3-shaped Q (B=1, H=32, n=32768, d=128, k=16: 1M rows), generated on the
+    device and coded by sfa_topk_codes, is bit-exact against the oracle on the host-regenerated Q."""
+    import torch
+    from helpers import gen_big
+    shape = (1, 32, 32768, 128)
+    qt = torch.empty(shape, dtype=torch.bfloat16, device="cuda")
+    lib.gen_fill(qt, 21, inputs.TID_Q)
+    gi, gv = lib.topk_codes(qt, 16)
+    torch.cuda.synchronize()
+    del qt
+    q_host = gen_big(21, inputs.TID_Q, shape, "bf16")
+    oi, ov = oracle_codes(q_host, 16)
+    np.testing.assert_array_equal(from_torch(gi), oi)
+    np.testing.assert_array_equal(from_torch(gv), ov)
