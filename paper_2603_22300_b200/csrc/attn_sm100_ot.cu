@@ -47,6 +47,12 @@ namespace {
 #ifndef SFA_OT_POLY
 #define SFA_OT_POLY 2
 #endif
+// P handed to the tensor core in two 64-key halves (PFULL/PEMPTY per half): P.V of the first half
+// runs while the softmax exponentiates the second, and the next tile's first half is stored as soon
+// as P.V has read that half.  0: one hand-off per 128-key tile (round 1).
+#ifndef SFA_OT_PHALF
+#define SFA_OT_PHALF 1
+#endif
 
 
 
@@ -469,9 +475,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                 }
                 if (h == 0) {
                     if (lane == 0 && wq == 0) TLREC(0x4000 | (t << 10) | (j & 1023));
+#if SFA_OT_PHALF
+                    // the rescale needs every P.V of tile j-1 complete (its second half is the last)
+                    if (rescale && j > 0) mbar_wait(BAR(PEMPTY + 1), (j & 1) ^ 1);
+#else
                     // P buffer j % NP free (its last P.V, of P(j - NP), complete)
                     mbar_wait(BAR(PEMPTY + j % C::NP), ((j / C::NP) & 1) ^ 1);
                     if (lane == 0 && wq == 0) TLREC(0x7000 | (t << 10) | (j & 1023));
+#endif
                     if (rescale && j > 0) {
                         named_bar_sync(bar_id, 128);  // every row's alpha is in f_t
                         tc_fence_after();
@@ -493,17 +504,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                         tmem_st_wait();
                     }
                 }
+#if SFA_OT_PHALF
+                // half h of the P buffer is free once P.V(j-1, h) has read it
+                mbar_wait(BAR(PEMPTY + h), (j & 1) ^ 1);
+                if (h == 0 && lane == 0 && wq == 0) TLREC(0x7000 | (t << 10) | (j & 1023));
+#endif
                 // P row (t*128 + r), atom h: 16-byte chunk c8 swizzled by row
 #pragma unroll
                 for (int c8 = 0; c8 < 8; ++c8)
                     sts_v4(prow + (uint32_t)(j % C::NP) * C::PT + (uint32_t)h * (2 * BM * 128) + ((uint32_t)(c8 ^ (r & 7)) << 4), pk[4 * c8], pk[4 * c8 + 1],
                            pk[4 * c8 + 2], pk[4 * c8 + 3]);
+#if SFA_OT_PHALF
+                // hand half h to the tensor core now: P.V(j, 0) runs while half 1 is exponentiated
+                fence_proxy_async_smem();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(BAR(PFULL + h));
+#endif
             }
             l += rs0 + rs1;
+#if !SFA_OT_PHALF
             fence_proxy_async_smem();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(BAR(PFULL + j % C::NP));
+#endif
             if (lane == 0 && wq == 0) TLREC(0x2000 | (t << 10) | (j & 1023));
         }
         // ---- epilogue (step 8): O = 2^e (sum_j P'_j V'_j) / l, V' = V 2^-e (vprep.cu)
@@ -620,11 +645,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                         umma_commit(BAR(KEMPTY + s1));
                     }
                     mbar_wait(BAR(VFULL), j & 1);  // NV == 1 here
+#if SFA_OT_PHALF
+                    // O^T += V(j)^T P(j)^T in two 64-key halves, each as soon as both tiles stored it
+                    for (int h = 0; h < 2; ++h) {
+                        mbar_wait(BAR(PFULL + h), j & 1);
+                        if (h == 0) TLREC(0x3000 | (j & 1023));
+                        tc_fence_after();
+                        const uint32_t va = sbase + C::OFF_V, pa = sbase + C::OFF_P + h * (2 * BM * 128);
+#pragma unroll
+                        for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
+                            umma_ss(tmem + C::O_COL, umma_desc_sw128(va + kk * 2048, BN * 128, 1024),
+                                    umma_desc_sw128(pa + (kk & 3) * 32, 16, 1024), idO, (j > 0 || kk > 0) ? 1u : 0u);
+                        umma_commit(BAR(PEMPTY + h));
+                    }
+#else
                     mbar_wait(BAR(PFULL), j & 1);
                     TLREC(0x3000 | (j & 1023));
                     tc_fence_after();
                     mma_O(j > 0, 0, 0);
                     umma_commit(BAR(PEMPTY));
+#endif
                     umma_commit(BAR(VEMPTY));
                 }
                 umma_commit(BAR(OFULL));
