@@ -47,12 +47,13 @@ namespace {
 #ifndef SFA_OT_POLY
 #define SFA_OT_POLY 2
 #endif
-// P handed to the tensor core in two 64-key halves (PFULL/PEMPTY per half): P.V of the first half
-// runs while the softmax exponentiates the second, and the next tile's first half is stored as soon
-// as P.V has read that half.  0: one hand-off per 128-key tile (round 1).
+// 1: P handed to the tensor core in two 64-key halves (PFULL/PEMPTY per half): P.V of the first half
+// runs while the softmax exponentiates the second.  Measured slower at Qwen3-32K (attention 7.51-7.59 ms
+// vs 7.08-7.12 ms with one hand-off per tile, same box, profiles/r02_phalf_ab.txt), so off by default.
 #ifndef SFA_OT_PHALF
-#define SFA_OT_PHALF 1
+#define SFA_OT_PHALF 0
 #endif
+
 
 
 
@@ -583,9 +584,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         const int64_t kv0 = ((int64_t)b * p.H_kv + g) * p.n_kv;
         for (int j = 0; j < nt; ++j) {
             const int s = j % C::NK, u = j / C::NK;
+            mbar_wait(BAR(KEMPTY + s), (u & 1) ^ 1);
             const int64_t key = (int64_t)(j0 + j) * BN + r;
             const bool ok = key < p.n_kv;
-            mbar_wait(BAR(KEMPTY + s), (u & 1) ^ 1);
             densify_row<D>(sbase + C::OFF_K + s * C::KT, BN, r, ok, p.k_idx + (kv0 + key) * k, kv + (kv0 + key) * k, k);
             fence_proxy_async_smem();
             __syncwarp();

@@ -63,7 +63,9 @@ __global__ void f2fp_kernel(float *out, int iters, long long *clk) {
     if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
 }
 
-// 2 ex2 + 1 f16x2 pack per pair, the softmax's mix
+// 2 ex2 + 1 f16x2 pack per pair, the softmax's mix.  Each ex2 feeds the next iteration (x <- -ex2(x)),
+// otherwise ptxas hoists the loop-invariant MUFU ops out of the loop (an earlier version of this test
+// reported 254 "ex2/clk" that way).
 template <int ILP>
 __global__ void mix_kernel(float *out, int iters, long long *clk) {
     float v[2 * ILP];
@@ -80,10 +82,34 @@ __global__ void mix_kernel(float *out, int iters, long long *clk) {
             asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(b) : "f"(v[2 * i + 1]));
             asm volatile("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(a), "f"(b));
             acc ^= r;
+            v[2 * i] = -a;
+            v[2 * i + 1] = -b;
         }
     }
     long long t1 = clock64();
     if (acc == 12345u) out[0] = 1.f;
+    if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
+}
+
+// MUFU.EX2 on f16x2 (ex2.approx.f16x2): ptxas emits two MUFU.EX2.F16 per instruction on sm_100a
+template <int ILP>
+__global__ void ex2h2_kernel(float *out, int iters, long long *clk) {
+    uint32_t v[ILP];
+#pragma unroll
+    for (int i = 0; i < ILP; ++i) v[i] = 0xBC00BC00u ^ (threadIdx.x + i);
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < ILP; ++i) {
+            asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(v[i]));
+            v[i] ^= 0x80008000u;  // keep the argument negative
+        }
+    }
+    long long t1 = clock64();
+    uint32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < ILP; ++i) s ^= v[i];
+    if (s == 12345u) out[0] = 1.f;
     if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
 }
 
@@ -113,6 +139,7 @@ int main() {
         run("fma.rn.f32x2 ILP8 (elems)", ffma2_kernel<8>, th, 16, 4096);
         run("cvt.rn.f16x2.f32 ILP8 (instr)", f2fp_kernel<8>, th, 8, 4096);
         run("2 ex2 + 1 cvt f16x2 (ex2/clk)", mix_kernel<8>, th, 16, 4096);
+        run("ex2.approx.f16x2 ILP8 (elems)", ex2h2_kernel<8>, th, 16, 4096);
     }
     return 0;
 }
