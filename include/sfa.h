@@ -66,8 +66,11 @@ typedef enum {
     SFA_KERNEL_DECODE = 5,     /* few query rows over a long cache (n_q * H / H_kv <= 16, bf16): split-KV
                                   CUDA-core kernel reading codes + V, LSE merge.  AUTO picks
                                   it for such shapes.                                                      */
-    SFA_KERNEL_SM100_OT = 6    /* SM100 with a transposed output accumulator: O^T += V^T P^T as N = 256 MMAs
+    SFA_KERNEL_SM100_OT = 6,   /* SM100 with a transposed output accumulator: O^T += V^T P^T as N = 256 MMAs
                                   over both query tiles, P in shared memory (bf16, d_v = 128)              */
+    SFA_KERNEL_SM100_PP = 7    /* two query tiles in ping-pong: K~ tiles by TMA from key rows decompressed
+                                  once per key (prepare step), P in TMEM (TS-MMA P.V), exponential phases
+                                  of the two softmax warpgroups alternating (bf16, R1, no window)          */
 } sfa_kernel;
 
 SFA_API const char *sfa_status_string(sfa_status s);

@@ -28,11 +28,11 @@ sfa_status validate_desc(const sfa_attn_desc *d) {
     if (d->causal != 0 && d->causal != 1) return SFA_ERR_INVALID_ARGUMENT;
     if (!(d->scale > 0.f) || !isfinite(d->scale)) return SFA_ERR_INVALID_ARGUMENT;
     if (d->dtype != SFA_F32 && d->dtype != SFA_BF16) return SFA_ERR_INVALID_ARGUMENT;
-    if (d->kernel < SFA_KERNEL_AUTO || d->kernel > SFA_KERNEL_SM100_OT) return SFA_ERR_INVALID_ARGUMENT;
+    if (d->kernel < SFA_KERNEL_AUTO || d->kernel > SFA_KERNEL_SM100_PP) return SFA_ERR_INVALID_ARGUMENT;
     if (d->d != 64 && d->d != 128) return SFA_ERR_UNSUPPORTED;
     if (d->d_v != 64 && d->d_v != 128) return SFA_ERR_UNSUPPORTED;
     if ((d->kernel == SFA_KERNEL_SM100 || d->kernel == SFA_KERNEL_SM100_PAIR || d->kernel == SFA_KERNEL_SM100_WIDE ||
-         d->kernel == SFA_KERNEL_SM100_OT) &&
+         d->kernel == SFA_KERNEL_SM100_OT || d->kernel == SFA_KERNEL_SM100_PP) &&
         d->dtype != SFA_BF16)
         return SFA_ERR_UNSUPPORTED;
     if ((d->kernel == SFA_KERNEL_SM100_PAIR || d->kernel == SFA_KERNEL_SM100_OT) && d->d_v != 128) return SFA_ERR_UNSUPPORTED;
@@ -83,13 +83,25 @@ size_t vprep_amax_bytes(const sfa_attn_desc *d) { return align_up((int64_t)d->B 
 size_t vprep_bytes(const sfa_attn_desc *d) {
     return vprep_amax_bytes(d) + (size_t)d->B * d->H_kv * d->n_kv * d->d_v * 2;
 }
-// R2 on SM100_OT: the key-tile feature bitsets (edges.cu) follow the V prep, 256-aligned
+// SM100_OT: the decompressed K~ rows (bf16, read by TMA) follow the V prep, 256-aligned; then, for R2,
+// the key-tile feature bitsets (edges.cu)
+bool uses_kdense(const sfa_attn_desc *d) {
+    const int k = resolve_kernel(d);
+    return k == SFA_KERNEL_SM100_OT || k == SFA_KERNEL_SM100_PP;
+}
+size_t kdense_off(const sfa_attn_desc *d) { return align_up(vprep_bytes(d), 256); }
+size_t kdense_bytes(const sfa_attn_desc *d) {
+    return uses_kdense(d) ? align_up((int64_t)d->B * d->H_kv * d->n_kv * d->d * 2, 256) : 0;
+}
 bool uses_kmask(const sfa_attn_desc *d) { return d->edges_only && resolve_kernel(d) == SFA_KERNEL_SM100_OT; }
 size_t ws_bytes(const sfa_attn_desc *d) {
     const int kern = resolve_kernel(d);
     if (kern == SFA_KERNEL_SIMT) return bucket_bytes(d);
     if (kern == SFA_KERNEL_DECODE) return decode_workspace_bytes((int64_t)d->B * d->H_kv, d->n_kv, d->d_v);
-    if (uses_kmask(d)) return align_up(vprep_bytes(d), 256) + kfmask_bytes((int64_t)d->B * d->H_kv, d->n_kv, d->d);
+    if (uses_kdense(d)) {
+        const size_t o = kdense_off(d) + kdense_bytes(d);
+        return uses_kmask(d) ? o + kfmask_bytes((int64_t)d->B * d->H_kv, d->n_kv, d->d) : o;
+    }
     return vprep_bytes(d);
 }
 
@@ -126,7 +138,8 @@ AttnParams make_params(const sfa_attn_desc *d, const uint8_t *q_idx, const void 
     p.L = layout_of(d);
     p.edges_only = d->edges_only;
     p.window = d->window;
-    p.kfmask = (ws && uses_kmask(d)) ? (const uint32_t *)((const uint8_t *)ws + align_up(vprep_bytes(d), 256)) : nullptr;
+    p.k_dense = (ws && uses_kdense(d)) ? (const uint8_t *)ws + kdense_off(d) : nullptr;
+    p.kfmask = (ws && uses_kmask(d)) ? (const uint32_t *)((const uint8_t *)ws + kdense_off(d) + kdense_bytes(d)) : nullptr;
     return p;
 }
 
@@ -146,6 +159,8 @@ sfa_status run_prepare(const sfa_attn_desc *d, const uint8_t *k_idx, const void 
         return from_cuda(launch_bucket(k_idx, k_val, d->dtype == SFA_BF16, d->d, d->k, (int64_t)d->B * d->H_kv,
                                        d->n_kv, p.L, ws, st));
     cudaError_t e = launch_vprep(v, (int64_t)d->B * d->H_kv, d->n_kv, d->d_v, (uint32_t *)p.v_amax, (void *)p.v16, st);
+    if (e == cudaSuccess && uses_kdense(d))
+        e = launch_kdense(k_idx, k_val, (int64_t)d->B * d->H_kv * d->n_kv, d->d, d->k, (void *)p.k_dense, st);
     if (e == cudaSuccess && uses_kmask(d))
         e = launch_kfmask(k_idx, (int64_t)d->B * d->H_kv, d->n_kv, d->d, d->k, (uint32_t *)p.kfmask, st);
     return from_cuda(e);
@@ -161,6 +176,7 @@ sfa_status run_attn_prepared(const sfa_attn_desc *d, const uint8_t *q_idx, const
     if (kern == SFA_KERNEL_SM100_PAIR) return from_launch(launch_attn_sm100_pair(p, d->d, d->d_v, st, dbg));
     if (kern == SFA_KERNEL_SM100_WIDE) return from_launch(launch_attn_sm100_wide(p, d->d, d->d_v, st, dbg));
     if (kern == SFA_KERNEL_SM100_OT) return from_launch(launch_attn_sm100_ot(p, d->d, d->d_v, st, dbg));
+    if (kern == SFA_KERNEL_SM100_PP) return from_launch(launch_attn_sm100_pp(p, d->d, d->d_v, st, dbg));
     if (kern == SFA_KERNEL_SM100) return from_launch(launch_attn_sm100(p, d->d, d->d_v, st, dbg));
     return from_cuda(launch_attn_simt(p, d->dtype == SFA_BF16, d->d, d->d_v, st));
 }

@@ -28,6 +28,7 @@
 // Shared memory (d = 128): Q~ 2 x 32 KB, K~ 2 x 32 KB, V 32 KB, P 64 KB (256 rows x 128 keys fp16,
 // K-major SW128), 1 KB per-query factors; 226 KB of the 227 KB.
 #include <cudaTypedefs.h>
+#include <cstring>
 #include <mutex>
 
 #include "densify.cuh"
@@ -52,6 +53,13 @@ namespace {
 // vs 7.08-7.12 ms with one hand-off per tile, same box, profiles/r02_phalf_ab.txt), so off by default.
 #ifndef SFA_OT_PHALF
 #define SFA_OT_PHALF 0
+#endif
+// 1: the K~ ring is filled by TMA from the decompressed key rows the prepare step writes once per key
+// (k_dense_kernel, vprep.cu); 0: the decompression warps rebuild every K~ tile in shared memory from the
+// codes (zero fill + k u16 stores per key per work item: ~630 of the ~3,200 shared-memory wavefronts of
+// a key-tile iteration, profiles/r02_ot_ab.txt)
+#ifndef SFA_OT_KTMA
+#define SFA_OT_KTMA 1
 #endif
 
 
@@ -182,6 +190,7 @@ __device__ __forceinline__ void prefetch_l1(const void *ptr) {
 // WIN: causal sliding window (N4) -- a template flag so the full-causal kernel carries none of its work.
 template <int D, bool DBG, bool EDGE, bool FUSEQ, bool WIN>
 __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid_constant__ CUtensorMap tmap_v,
+                                                                      const __grid_constant__ CUtensorMap tmap_k,
                                                                       const OtArgs a) {
     using C = Cfg<D>;
     const AttnParams &p = a.p;
@@ -221,7 +230,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
     if (threadIdx.x == 0) {
         for (int i = 0; i < NBAR; ++i) {
             uint32_t cnt = 1;
-            if (i == KFULL || i == KFULL + 1 || i == SEMPTY || i == SEMPTY + 1 || i == QFULL) cnt = 4;
+            if ((!SFA_OT_KTMA && (i == KFULL || i == KFULL + 1)) || i == SEMPTY || i == SEMPTY + 1 || i == QFULL) cnt = 4;
             if (FUSEQ && i == QFULL) cnt = 8;  // the eight softmax warps build Q~
             if (i == PFULL || i == PFULL + 1) cnt = 8;
             mbar_init(BAR(i), cnt);
@@ -229,7 +238,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         fence_mbar_init();
     }
     if (warp == 12) tmem_alloc<512>(smem_u32(tmem_slot));
-    if (warp == 13 && lane == 0) tma_prefetch_desc(&tmap_v);
+    if (warp == 13 && lane == 0) {
+        tma_prefetch_desc(&tmap_v);
+        if (SFA_OT_KTMA) tma_prefetch_desc(&tmap_k);
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -582,7 +594,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
             if (lane == 0) mbar_arrive(BAR(QFULL));
         }
         const int64_t kv0 = ((int64_t)b * p.H_kv + g) * p.n_kv;
-        for (int j = 0; j < nt; ++j) {
+        for (int j = 0; j < (SFA_OT_KTMA ? 0 : nt); ++j) {
             const int s = j % C::NK, u = j / C::NK;
             mbar_wait(BAR(KEMPTY + s), (u & 1) ^ 1);
             const int64_t key = (int64_t)(j0 + j) * BN + r;
@@ -686,6 +698,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                 }
             }
             __syncwarp();
+        } else if (warp == 14 && SFA_OT_KTMA) {
+            // ============================ TMA producer for K~ (decompressed rows) ============================
+            if (lane == 0) {
+                const int bhkv = b * p.H_kv + g;
+                for (int j = 0; j < nt; ++j) {
+                    const int s = j % C::NK, u = j / C::NK;
+                    mbar_wait(BAR(KEMPTY + s), (u & 1) ^ 1);
+                    mbar_arrive_expect_tx(BAR(KFULL + s), C::KT);
+                    const uint32_t dst = sbase + C::OFF_K + s * C::KT;
+#pragma unroll
+                    for (int cb = 0; cb < D / 64; ++cb)
+                        tma_load_3d(dst + cb * BN * 128, &tmap_k, BAR(KFULL + s), cb * 64, (j0 + j) * BN, bhkv);
+                }
+            }
+            __syncwarp();
         }
     }
     tc_fence_before();
@@ -725,6 +752,18 @@ cudaError_t launch_t(const OtArgs &a, cudaStream_t stream, int items) {
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    CUtensorMap tk;  // K~ rows (bf16 [B*H_kv][n_kv][D]), same box shape and swizzle as the decompression wrote
+    memset(&tk, 0, sizeof(tk));
+    if (SFA_OT_KTMA) {
+        if (p.k_dense == nullptr) return cudaErrorInvalidValue;
+        cuuint64_t kdims[3] = {(cuuint64_t)D, (cuuint64_t)p.n_kv, (cuuint64_t)p.B * p.H_kv};
+        cuuint64_t kstrides[2] = {(cuuint64_t)D * 2, (cuuint64_t)p.n_kv * D * 2};
+        cuuint32_t kbox[3] = {64, BN, 1};
+        cr = encode(&tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(p.k_dense), kdims, kstrides, kbox, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
     const bool win = p.window > 0;
     auto kern = p.q_dense != nullptr ? attn_sm100_ot_kernel<D, false, false, true, false>
                 : win ? (p.edges_only ? attn_sm100_ot_kernel<D, false, true, false, true>
@@ -735,7 +774,7 @@ cudaError_t launch_t(const OtArgs &a, cudaStream_t stream, int items) {
                                                    : attn_sm100_ot_kernel<D, false, false, false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
-    kern<<<items, NTHREADS, C::SMEM, stream>>>(tm, a);
+    kern<<<items, NTHREADS, C::SMEM, stream>>>(tm, tk, a);
     return cudaGetLastError();
 }
 

@@ -12,6 +12,7 @@ struct AttnParams {
     const void *v;
     const void *v16;         // sm100: fp16 copy of V scaled by 2^-e per (b, kv head) (vprep.cu)
     const uint32_t *v_amax;  // sm100: per (b, kv head) max|V| bits, e = vprep_head_exp(bits)
+    const void *k_dense = nullptr;  // SM100_OT: decompressed K~ rows, bf16 [B][H_kv][n_kv][d] (vprep.cu)
     void *o;
     float *lse;
     const uint8_t *ws;
@@ -51,6 +52,9 @@ __device__ __forceinline__ int vprep_head_exp(uint32_t amax_bits) {
     const int e = (int)((amax_bits >> 23) & 0xFF) - 127 - 14;
     return e < -126 ? -126 : e;
 }
+// K~ rows from the key codes, bf16 [rows][d] (vprep.cu k_dense_kernel), for the SM100_OT K~ TMA
+cudaError_t launch_kdense(const uint8_t *k_idx, const void *k_val, int64_t rows, int d, int k, void *out,
+                          cudaStream_t stream);
 // decode shape (rows = n_q * H / H_kv <= 16 per kv head): split-KV CUDA-core kernel + LSE merge
 // (decode.cu); ws >= decode_workspace_bytes
 cudaError_t launch_decode(const AttnParams &p, int d, int d_v, cudaStream_t st, void *ws);
@@ -65,6 +69,8 @@ cudaError_t launch_attn_sm100_pair(const AttnParams &p, int d, int d_v, cudaStre
 // the same forward with 256-key score tiles and P apart from S (attn_sm100_wide.cu)
 cudaError_t launch_attn_sm100_wide(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
 cudaError_t launch_attn_sm100_ot(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
+// two query tiles in ping-pong, K~ by TMA from p.k_dense, P in TMEM (attn_sm100_pp.cu); R1, no window
+cudaError_t launch_attn_sm100_pp(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
 // backward with the straight-through rule (bwd.cu): D = rowsum(dO . O) into Dws [B*H*n_q], then the
 // dK~/dV and dQ~ tensor-core kernels; gradients w.r.t. the code values and V, fp32
 cudaError_t launch_attn_bwd(const AttnParams &p, int d, int d_v, const void *dO, float *Dws, float *dq, float *dk,

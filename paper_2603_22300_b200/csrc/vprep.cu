@@ -60,7 +60,59 @@ __global__ void __launch_bounds__(256) v_to_f16_kernel(const uint4 *__restrict__
     }
 }
 
+// K~ for the SM100_OT kernel's TMA: the decompressed key rows, bf16 [rows][D], written once per key
+// (the attention kernel would otherwise rebuild every key tile in shared memory once per work item,
+// ~630 shared-memory wavefronts per key tile, profiles/r02_ot_ab.txt).  Bit copies of the code values
+// at their indices, zeros elsewhere.  A CTA stages 128 rows in shared memory (zero fill,
+// thread per row scatters its k values), then writes them out with coalesced 16-byte stores.
+constexpr int KD_ROWS = 128;
+template <int D>
+__global__ void __launch_bounds__(KD_ROWS) k_dense_kernel(const uint8_t *__restrict__ idx,
+                                                           const uint16_t *__restrict__ val, int64_t rows, int k,
+                                                           uint4 *__restrict__ out) {
+    constexpr int NC = D / 8;  // 16-byte chunks per row
+    extern __shared__ uint4 kd_sm[];  // [KD_ROWS][NC]
+    const int t = threadIdx.x;
+    const int64_t row0 = (int64_t)blockIdx.x * KD_ROWS;
+    const int nrows = (int)((rows - row0) < KD_ROWS ? (rows - row0) : KD_ROWS);
+    for (int v = t; v < KD_ROWS * NC; v += KD_ROWS) kd_sm[v] = make_uint4(0u, 0u, 0u, 0u);
+    __syncthreads();
+    if (t < nrows) {
+        uint16_t *row = reinterpret_cast<uint16_t *>(kd_sm + t * NC);
+        const uint8_t *ir = idx + (row0 + t) * k;
+        const uint16_t *vr = val + (row0 + t) * k;
+        if ((k & 7) == 0) {
+            for (int e0 = 0; e0 < k; e0 += 8) {
+                const uint2 ii = __ldg(reinterpret_cast<const uint2 *>(ir + e0));
+                const uint4 vv = __ldg(reinterpret_cast<const uint4 *>(vr + e0));
+                const uint32_t iw[2] = {ii.x, ii.y}, vw[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    row[(iw[e >> 2] >> (8 * (e & 3))) & 0xFFu] = (uint16_t)(vw[e >> 1] >> (16 * (e & 1)));
+            }
+        } else {
+            for (int e = 0; e < k; ++e) row[__ldg(ir + e)] = __ldg(vr + e);
+        }
+    }
+    __syncthreads();
+    uint4 *dst = out + row0 * NC;
+    for (int v = t; v < nrows * NC; v += KD_ROWS) dst[v] = kd_sm[v];
+}
+
 }  // namespace
+
+cudaError_t launch_kdense(const uint8_t *k_idx, const void *k_val, int64_t rows, int d, int k, void *out,
+                          cudaStream_t stream) {
+    if (rows == 0) return cudaSuccess;
+    const int64_t blocks = (rows + KD_ROWS - 1) / KD_ROWS;
+    if (blocks > 0x7FFFFFFF) return cudaErrorInvalidValue;
+    const size_t smem = (size_t)KD_ROWS * d * 2;
+    if (d == 64)
+        k_dense_kernel<64><<<(unsigned)blocks, KD_ROWS, smem, stream>>>(k_idx, (const uint16_t *)k_val, rows, k, (uint4 *)out);
+    else
+        k_dense_kernel<128><<<(unsigned)blocks, KD_ROWS, smem, stream>>>(k_idx, (const uint16_t *)k_val, rows, k, (uint4 *)out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_vprep(const void *v, int64_t bh_kv, int64_t n_kv, int d_v, uint32_t *amax, void *v16,
                          cudaStream_t stream) {

@@ -62,9 +62,13 @@ def test_desc_validation(sfa):
     L = sfa.lib()
     ok = desc(sfa, kernel=sfa.KERNEL_SIMT)
     assert L.sfa_attn_workspace_bytes(ctypes.byref(ok)) > 0
-    # the sm_100a kernel decompresses key codes on chip (no buckets); its workspace is the
-    # 256-aligned max|V| per (b, kv head) + the fp16 copy of V (reading A12)
-    assert L.sfa_attn_workspace_bytes(ctypes.byref(desc(sfa))) == 256 + 1 * 2 * 300 * 128 * 2
+    # the default sm_100a kernel (SM100_OT, no buckets): the 256-aligned max|V| per (b, kv head) + the
+    # fp16 copy of V (reading A12), then 256-aligned, the decompressed bf16 K~ rows its TMA reads
+    v16 = 256 + 1 * 2 * 300 * 128 * 2
+    kd = 1 * 2 * 300 * 128 * 2
+    assert L.sfa_attn_workspace_bytes(ctypes.byref(desc(sfa))) == (v16 + 255) // 256 * 256 + (kd + 255) // 256 * 256
+    # SM100 (d_v = 64 default) decompresses the key codes on chip: V prep only
+    assert L.sfa_attn_workspace_bytes(ctypes.byref(desc(sfa, kernel=sfa.KERNEL_SM100))) == v16
     bad = [dict(H=3, H_kv=2), dict(k=0), dict(k=129), dict(n_q=0), dict(n_kv=0), dict(scale=-1.0),
            dict(scale=float("inf")), dict(q_pos0=-1)]
     for b in bad:

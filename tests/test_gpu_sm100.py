@@ -83,11 +83,12 @@ def test_peaked_rows_trigger_rescale(lib):
 # ---------------------------------------------------------------------------------------------
 # M = 256 CTA-pair kernel (attn_sm100_pair.cu): same checks
 # ---------------------------------------------------------------------------------------------
-VARIANTS = ["pair", "wide", "ot"]  # SFA_KERNEL_SM100_PAIR / _WIDE / _OT
+VARIANTS = ["pair", "wide", "ot", "pp"]  # SFA_KERNEL_SM100_PAIR / _WIDE / _OT / _PP
 
 
 def _kern(lib, name):
-    return {"pair": lib.KERNEL_SM100_PAIR, "wide": lib.KERNEL_SM100_WIDE, "ot": lib.KERNEL_SM100_OT}[name]
+    return {"pair": lib.KERNEL_SM100_PAIR, "wide": lib.KERNEL_SM100_WIDE, "ot": lib.KERNEL_SM100_OT,
+            "pp": lib.KERNEL_SM100_PP}[name]
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
@@ -114,7 +115,7 @@ def test_variant_score_tile_is_exact_overlap_sum(lib, variant, d, k):
     (2, 2, 2, 300, 64, 128, 8),     # MHA, d = 64, ragged
     (1, 2, 1, 515, 128, 128, 32),
     (1, 2, 2, 1, 128, 128, 4),      # a single token
-    (1, 2, 2, 700, 64, 64, 8),      # d_v = 64 (wide only)
+    (1, 2, 2, 700, 64, 64, 8),      # d_v = 64 (wide, pp)
 ])
 @pytest.mark.parametrize("causal", [True, False])
 def test_variant_against_oracle(lib, variant, shape, causal):

@@ -13,7 +13,8 @@ sys.path.insert(0, ROOT)
 from paper_2603_22300_b200 import inputs, sfa  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
-kern = {"sm100": sfa.KERNEL_SM100, "pair": sfa.KERNEL_SM100_PAIR, "wide": sfa.KERNEL_SM100_WIDE, "ot": sfa.KERNEL_SM100_OT}[sys.argv[2] if len(sys.argv) > 2 else "sm100"]
+kern = {"sm100": sfa.KERNEL_SM100, "pair": sfa.KERNEL_SM100_PAIR, "wide": sfa.KERNEL_SM100_WIDE, "ot": sfa.KERNEL_SM100_OT,
+        "pp": sfa.KERNEL_SM100_PP}[sys.argv[2] if len(sys.argv) > 2 else "sm100"]
 qwen = len(sys.argv) > 3 and sys.argv[3] == "qwen"  # bench config: causal, H=32, H_kv=8 (item 0 = last q block)
 B, H, H_kv, d, d_v, k = (1, 32, 8, 128, 128, 16) if qwen else (1, 2, 1, 128, 128, 16)
 dev = "cuda"
@@ -38,6 +39,18 @@ for tg, c in zip(tag, clk):
     kind, t, u = tg >> 12, (tg >> 10) & 3, tg & 1023
     ev[(names[kind], t, u)] = c
 nu = max(u for (_, _, u) in ev) + 1
+if len(sys.argv) > 2 and sys.argv[2] == "pp":  # ping-pong kernel: S ready, max done, turn, P stored, MMA saw P
+    print(f"{cnt} records, {nu} key tiles; clocks relative to the first record")
+    print("  j | tile 0: Srdy  maxd  turn  Pst   mmaP  | tile 1: Srdy  maxd  turn  Pst   mmaP  | exp0  exp1 | period")
+    prev = None
+    for u in range(nu):
+        r0 = [ev.get((nm, 0, u), -1) for nm in ("S_ready", "max_done", "max", "P_stored", "mma_sawP")]
+        r1 = [ev.get((nm, 1, u), -1) for nm in ("S_ready", "max_done", "max", "P_stored")] + [ev.get(("mma_sawP", 1, u), -1)]
+        per = r0[0] - prev if prev is not None else 0
+        prev = r0[0]
+        print(f"{u:3d} | " + " ".join(f"{x:6d}" for x in r0) + " | " + " ".join(f"{x:6d}" for x in r1) +
+              f" | {r0[3]-r0[2]:5d} {r1[3]-r1[2]:5d} | {per}")
+    sys.exit(0)
 print(f"{cnt} records, {nu} key tiles; clocks relative to the first record")
 print(" j | S0rdy  P0st  mmaP  | S1rdy  P1st  issued | softmax0 softmax1 | max0 max1 | period(S0rdy)")
 prev = None
