@@ -48,6 +48,10 @@ def parse():
     ap.add_argument("--edges-only", action="store_true",
                     help="reading A1/R2 (SURVEY 8(f) N4): only pairs whose supports intersect enter the softmax")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--separate-topk", action="store_true",
+                    help="stage 1 as two launches (Q, then K) instead of one sfa_topk_codes_qk launch")
+    ap.add_argument("--graph", action="store_true",
+                    help="time the step as one CUDA graph replay (stage split from an extra eager pass)")
     ap.add_argument("--concurrent-stages", action="store_true",
                     help="stage 1 on K and step 3 on a second stream concurrently with stage 1 on Q (measured: no "
                          "gain, the top-k kernels compete for the SMs); default: back to back on one stream")
@@ -665,7 +669,16 @@ def main():
     def step(ev=None):
         # stage 1 on Q, stage 1 on K, step 3 (V prep for sm100 / buckets for simt), steps 4-8 attention
         if ev: ev[0].record()
-        if not args.concurrent_stages:
+        if not args.concurrent_stages and not fused_q and not args.separate_topk:
+            # stage 1 on Q and on K in one launch (sfa_topk_codes_qk); stage slot 1 stays empty
+            r1 = L.sfa_topk_codes_qk(P(Q), B * H * n, d, P(q_idx), P(q_val), P(K), B * H_kv * n, d, P(k_idx),
+                                     P(k_val), dcode, d, k, P(status), st())
+            r2 = 0
+            if ev: ev[1].record()
+            if ev: ev[2].record()
+            r3 = L.sfa_attn_prepare(ctypes.byref(desc), P(k_idx), P(k_val), P(V), P(ws), ws.numel(), st())
+            if ev: ev[3].record()
+        elif not args.concurrent_stages:
             r1 = 0 if fused_q else L.sfa_topk_codes(P(Q), dcode, B * H * n, d, d, k, P(q_idx), P(q_val), P(status), st())
             if ev: ev[1].record()
             r2 = L.sfa_topk_codes(P(K), dcode, B * H_kv * n, d, d, k, P(k_idx), P(k_val), P(status), st())
@@ -709,18 +722,41 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    graph = None
+    if args.graph:  # the whole step as one CUDA graph (launch gaps of the 4-6 kernels collapse)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        for _ in range(2):
+            graph.replay()
+        torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         t_wall0 = time.perf_counter()
         for i in range(args.steps):
             flush.zero_()  # L2 flush: outside the step's events
-            step(evs[i])
+            if graph is not None:
+                evs[i][0].record()
+                graph.replay()
+                evs[i][4].record()
+            else:
+                step(evs[i])
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall0
     if world > 1:
         dist.barrier()
+    if graph is not None:  # the step from the replays; the stage split from as many eager steps
+        tot_ms = sum(e[0].elapsed_time(e[4]) for e in evs)
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+        for e in evs:
+            kev[id(e)] = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        for i in range(args.steps):
+            flush.zero_()
+            step(evs[i])
+        torch.cuda.synchronize()
     per = [[e[j].elapsed_time(e[j + 1]) for j in range(4)] for e in evs]  # ms per stage per step
     step_ms = [sum(p) for p in per]
-    tot_ms = sum(step_ms)
+    if graph is None:
+        tot_ms = sum(step_ms)
     stage_ms = [sum(p[j] for p in per) / args.steps for j in range(4)]
     join_wait_ms = None
     if args.concurrent_stages:  # key path timed on its own stream; [1] + [2] of `per` are the join wait
@@ -798,6 +834,16 @@ def main():
         except Exception as ex:  # context is optional
             context = {"dense_sdpa_error": str(ex)[:200]}
 
+    qk_fused = not args.concurrent_stages and not fused_q and not args.separate_topk
+    # our kernels per step: stage 1 (1 fused launch, 2 separate, 1 for K when Q is fused into the attention),
+    # step 3 (sm100: max|V| + fp16 V, + the decompressed K~ rows for OT/PP, + R2 bitsets; simt: buckets),
+    # the attention kernel
+    kern_res = args.kernel if args.kernel != "auto" else ("ot" if d_v == 128 else "sm100")
+    launches_per_step = (1 if (qk_fused or fused_q) else 2) + 1
+    if W.dtype == "bf16" and args.kernel != "simt":
+        launches_per_step += 2 + int(kern_res in ("ot", "pp")) + int(bool(args.edges_only))
+    else:
+        launches_per_step += 1
     pk = peaks()
     attn_ms = stage_ms[3]
     pairs = B * H * accounting.causal_pairs(n, n, 0, W.causal, args.window)  # this rank's units
@@ -882,12 +928,15 @@ def main():
                 "vs_baseline": None, "dtype": W.dtype,
                 "data": "synthetic (seeded counter-based generator on device, DESIGN.md input recipe)",
                 "config": config_of(args, W, B_glob, world),
-                "stage_ms": {"topk_q": stage_ms[0], "topk_k": stage_ms[1], "prepare": stage_ms[2],
-                             "attn": stage_ms[3],
+                "stage_ms": ({"topk_qk": stage_ms[0]} if qk_fused else {"topk_q": stage_ms[0], "topk_k": stage_ms[1]}) |
+                            {"prepare": stage_ms[2], "attn": stage_ms[3],
                              "note": ("topk_k and prepare run on a second stream concurrently with topk_q; the step "
                                       f"waited {join_wait_ms:.4f} ms for them after topk_q")
                              if join_wait_ms is not None else "stages back to back on one stream; each stage's "
-                                                              "max over ranks"},
+                                                              "max over ranks" +
+                             ("; topk_qk = Q and K codes in one launch (sfa_topk_codes_qk)" if qk_fused else "") +
+                             ("; the step timed as CUDA graph replays, the stage split from as many eager steps"
+                              if args.graph else "")},
                 "interactions": E_total,
                 "interactions_per_s": E_total / (ms_per_step / 1e3) if E_total is not None else None,
                 "interactions_note": "exact E = sum over allowed pairs of |S_i & S_j| (P:L114-120), prefix counts "
@@ -895,7 +944,7 @@ def main():
                 "pairs_per_s": pairs_total / (ms_per_step / 1e3),
                 "wall_s_timed_region": t_wall,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": (5 + int(args.edges_only) - int(fused_q) if sm100 else 4) * args.steps,
+                "gpu_launches": launches_per_step * args.steps,
                 "clocks": clk.summary(), "context": context, "long_context": long_ctx}
         print(json.dumps(line), flush=True)
     if dist.is_initialized():

@@ -89,6 +89,15 @@ SFA_API const char *sfa_status_string(sfa_status s);
 SFA_API sfa_status sfa_topk_codes(const void *x, sfa_dtype dtype, int64_t rows, int32_t d, int64_t ld, int32_t k,
                           uint8_t *idx, void *val, uint32_t *status_word, sfa_stream_t stream);
 
+/* Stage 1 on Q and on K of one step in ONE launch (the same operator and arguments as two
+ * sfa_topk_codes calls; results bit-identical to them).  bf16 only takes the fused launch;
+ * fp32, k = d or unaligned rows fall back to two launches.  Argument errors of either tensor are
+ * reported before any launch. */
+SFA_API sfa_status sfa_topk_codes_qk(const void *q, int64_t q_rows, int64_t q_ld, uint8_t *q_idx, void *q_val,
+                                     const void *k, int64_t k_rows, int64_t k_ld, uint8_t *k_idx, void *k_val,
+                                     sfa_dtype dtype, int32_t d, int32_t kk, uint32_t *status_word,
+                                     sfa_stream_t stream);
+
 /* ------------------------------------------------------------------------------------------
  * Stage 2: attention forward over the codes.
  * ------------------------------------------------------------------------------------------ */

@@ -94,14 +94,16 @@ size_t kdense_bytes(const sfa_attn_desc *d) {
     return uses_kdense(d) ? align_up((int64_t)d->B * d->H_kv * d->n_kv * d->d * 2, 256) : 0;
 }
 bool uses_kmask(const sfa_attn_desc *d) { return d->edges_only && resolve_kernel(d) == SFA_KERNEL_SM100_OT; }
+// ... and last, 256 bytes for the persistent tile scheduler's work counter (SM100_OT)
+size_t sched_off(const sfa_attn_desc *d) {
+    const size_t o = kdense_off(d) + kdense_bytes(d);
+    return uses_kmask(d) ? align_up(o + kfmask_bytes((int64_t)d->B * d->H_kv, d->n_kv, d->d), 256) : o;
+}
 size_t ws_bytes(const sfa_attn_desc *d) {
     const int kern = resolve_kernel(d);
     if (kern == SFA_KERNEL_SIMT) return bucket_bytes(d);
     if (kern == SFA_KERNEL_DECODE) return decode_workspace_bytes((int64_t)d->B * d->H_kv, d->n_kv, d->d_v);
-    if (uses_kdense(d)) {
-        const size_t o = kdense_off(d) + kdense_bytes(d);
-        return uses_kmask(d) ? o + kfmask_bytes((int64_t)d->B * d->H_kv, d->n_kv, d->d) : o;
-    }
+    if (uses_kdense(d)) return sched_off(d) + 256;
     return vprep_bytes(d);
 }
 
@@ -139,6 +141,7 @@ AttnParams make_params(const sfa_attn_desc *d, const uint8_t *q_idx, const void 
     p.edges_only = d->edges_only;
     p.window = d->window;
     p.k_dense = (ws && uses_kdense(d)) ? (const uint8_t *)ws + kdense_off(d) : nullptr;
+    p.sched = (ws && uses_kdense(d)) ? (uint32_t *)((uint8_t *)const_cast<void *>(ws) + sched_off(d)) : nullptr;
     p.kfmask = (ws && uses_kmask(d)) ? (const uint32_t *)((const uint8_t *)ws + kdense_off(d) + kdense_bytes(d)) : nullptr;
     return p;
 }
@@ -223,6 +226,33 @@ sfa_status sfa_topk_codes(const void *x, sfa_dtype dtype, int64_t rows, int32_t 
     if (((uintptr_t)x % vec) || ((size_t)ld * esize(dtype)) % vec) return SFA_ERR_INVALID_ARGUMENT;
     if (status_word && ((uintptr_t)status_word & 3u)) return SFA_ERR_INVALID_ARGUMENT;
     return from_cuda(launch_topk(x, dtype == SFA_BF16, rows, d, ld, k, idx, val, status_word, (cudaStream_t)stream));
+}
+
+sfa_status sfa_topk_codes_qk(const void *q, int64_t q_rows, int64_t q_ld, uint8_t *q_idx, void *q_val, const void *k,
+                             int64_t k_rows, int64_t k_ld, uint8_t *k_idx, void *k_val, sfa_dtype dtype, int32_t d,
+                             int32_t kk, uint32_t *status_word, sfa_stream_t stream) {
+    if (dtype != SFA_BF16) {  // the fp32 path has no fused launch: two stage-1 calls
+        sfa_status s = sfa_topk_codes(q, dtype, q_rows, d, q_ld, kk, q_idx, q_val, status_word, stream);
+        return s != SFA_OK ? s : sfa_topk_codes(k, dtype, k_rows, d, k_ld, kk, k_idx, k_val, status_word, stream);
+    }
+    // same argument rules as sfa_topk_codes, for each tensor, before any launch
+    for (int t = 0; t < 2; ++t) {
+        const void *x = t ? k : q;
+        const int64_t rows = t ? k_rows : q_rows, ld = t ? k_ld : q_ld;
+        const void *ix = t ? (const void *)k_idx : (const void *)q_idx, *vx = t ? k_val : q_val;
+        if (rows < 0 || d < 1 || d > 256 || kk < 1 || kk > d || ld < d) return SFA_ERR_INVALID_ARGUMENT;
+        if (d != 64 && d != 128) return SFA_ERR_UNSUPPORTED;
+        if (rows > 0 && (!x || !ix || !vx)) return SFA_ERR_INVALID_ARGUMENT;
+        const size_t vec = (size_t)(d / 32) * 2;
+        if (rows > 0 && (((uintptr_t)x % vec) || ((size_t)ld * 2) % vec)) return SFA_ERR_INVALID_ARGUMENT;
+    }
+    if (status_word && ((uintptr_t)status_word & 3u)) return SFA_ERR_INVALID_ARGUMENT;
+    if (q_rows == 0 || k_rows == 0) {
+        sfa_status s = sfa_topk_codes(q, dtype, q_rows, d, q_ld, kk, q_idx, q_val, status_word, stream);
+        return s != SFA_OK ? s : sfa_topk_codes(k, dtype, k_rows, d, k_ld, kk, k_idx, k_val, status_word, stream);
+    }
+    return from_cuda(launch_topk_pair(q, q_rows, q_ld, q_idx, q_val, k, k_rows, k_ld, k_idx, k_val, d, kk, status_word,
+                                      (cudaStream_t)stream));
 }
 
 size_t sfa_attn_workspace_bytes(const sfa_attn_desc *desc) {

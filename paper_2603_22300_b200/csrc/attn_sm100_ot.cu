@@ -48,19 +48,21 @@ namespace {
 #ifndef SFA_OT_POLY
 #define SFA_OT_POLY 2
 #endif
-// 1: P handed to the tensor core in two 64-key halves (PFULL/PEMPTY per half): P.V of the first half
-// runs while the softmax exponentiates the second.  Measured slower at Qwen3-32K (attention 7.51-7.59 ms
-// vs 7.08-7.12 ms with one hand-off per tile, same box, profiles/r02_phalf_ab.txt), so off by default.
-#ifndef SFA_OT_PHALF
-#define SFA_OT_PHALF 0
-#endif
-// 1: the K~ ring is filled by TMA from the decompressed key rows the prepare step writes once per key
-// (k_dense_kernel, vprep.cu); 0: the decompression warps rebuild every K~ tile in shared memory from the
-// codes (zero fill + k u16 stores per key per work item: ~630 of the ~3,200 shared-memory wavefronts of
-// a key-tile iteration, profiles/r02_ot_ab.txt)
-#ifndef SFA_OT_KTMA
-#define SFA_OT_KTMA 1
-#endif
+// P is handed to the tensor core once per 128-key tile (two 64-key hand-offs measured slower: attention
+// 7.51-7.59 vs 7.08-7.12 ms, profiles/r02_ot_ab.txt).  The K~ ring is filled by TMA from the key rows
+// the prepare step decompresses once per key (k_dense_kernel, vprep.cu): rebuilding every K~ tile in
+// shared memory once per work item cost ~630 of the ~3,200 shared-memory wavefronts of a key-tile
+// iteration (6.93 -> 6.53 ms, profiles/r02_ot_ab.txt).
+//
+// Tile scheduler: persistent CTAs (one per SM) take work items dynamically -- CTA c starts with item c,
+// then its K~ producer warp claims the next unclaimed item (atomicAdd on a counter in the workspace)
+// and publishes it to the CTA's other roles through a 4-slot ring in shared memory.  The item list is
+// in kv-group-major, heaviest-causal-first order, so this is greedy LPT (simulated 98 % balance at
+// Qwen3-32K vs 94 % for a static snake order, which measured 2 % slower than one item per CTA).
+// Every pipeline counter runs across items: the next
+// item's Q~ is built as soon as the current item's last S MMA has completed (QEMPTY), its first S MMAs
+// are issued during the current item's last softmax, its K~ / V tiles stream in meanwhile, and only
+// its first P.V waits for the current item's epilogue to have read O^T out of TMEM (OEMPTY).
 
 
 
@@ -84,7 +86,7 @@ struct Cfg {
     static constexpr int OFF_V = OFF_K + NK * KT;
     static constexpr int OFF_P = OFF_V + NV * VT;
     static constexpr int OFF_BAR = OFF_P + NP * PT;
-    static constexpr int OFF_F = OFF_BAR + 192;  // 2 x 128 fp32 per-query factors (alpha, then 1/l)
+    static constexpr int OFF_F = OFF_BAR + 256;  // 2 x 128 fp32 per-query factors (alpha, then 1/l)
     static constexpr int SMEM = OFF_F + 1024 + 1024;  // + slack to align the base to 1024 B
     static constexpr int O_COL = 256;
 };
@@ -93,8 +95,9 @@ static_assert(Cfg<128>::SMEM <= 232448, "shared memory budget");
 // mbarrier slots
 enum {
     KFULL = 0, KEMPTY = 2, VFULL = 4, VEMPTY = 6, SFULL = 8, SEMPTY = 10, PFULL = 12, PEMPTY = 14, OFULL = 16,
-    QFULL = 17, NBAR = 18
+    QFULL = 17, QEMPTY = 18, OEMPTY = 19, IFULL = 20, IEMPTY = 24, NBAR = 28
 };
+constexpr int NRING = 4;  // work-item ring slots
 
 struct OtArgs {
     AttnParams p;
@@ -102,6 +105,7 @@ struct OtArgs {
     int32_t pair_heads;  // 1: tiles (2hp, 2hp+1) at one q block; 0: (h, 2p), (h, 2p+1)
     int32_t per_rank;    // work items per q-block rank
     int32_t nkt;         // ceil(n_kv / BN)
+    int32_t items;       // work items (the persistent CTAs walk them, sched_item)
     float c_scale;       // scale * log2(e)
     float *dbg;          // optional: raw S of the first key tile of work item 0, tile 0 (tests)
 };
@@ -121,6 +125,10 @@ struct Tile {
 // major across every head (global LPT order, the earlier version).
 #ifndef SFA_OT_ORDER
 #define SFA_OT_ORDER 1
+#endif
+// 1: one work item per CTA (grid = items, the round-1 launch) instead of the persistent tile scheduler
+#ifndef SFA_OT_ONE_ITEM_PER_CTA
+#define SFA_OT_ONE_ITEM_PER_CTA 0
 #endif
 __device__ __forceinline__ void decode_item(const OtArgs &a, int item, int &b, Tile (&t)[2]) {
     const AttnParams &p = a.p;
@@ -162,6 +170,49 @@ __device__ __forceinline__ void decode_item(const OtArgs &a, int item, int &b, T
     }
 }
 
+// one work item's geometry: batch, kv group, its key tiles j0, j0 + 1, ..., j0 + nt - 1
+struct ItemGeo {
+    int b, g, nt, j0;
+    Tile tl[2];
+};
+template <bool WIN>
+__device__ __forceinline__ ItemGeo item_geo(const OtArgs &a, int item) {
+    const AttnParams &p = a.p;
+    ItemGeo G;
+    decode_item(a, item, G.b, G.tl);
+    G.g = G.tl[0].h / (p.H / p.H_kv);
+    int nt = a.nkt;
+    if (p.causal) {  // up to the diagonal of the item's last valid row
+        const int qbl = G.tl[1].valid ? G.tl[1].qb : G.tl[0].qb;
+        int64_t last = (int64_t)qbl * BM + BM - 1;
+        if (last > p.n_q - 1) last = p.n_q - 1;
+        const int64_t lim = (p.q_pos0 + last) / BN + 1;
+        if (lim < nt) nt = (int)lim;
+    }
+    // sliding window (N4): key tiles before the window of the item's first row are skipped
+    int j0 = 0;
+    if (WIN) {
+        const int64_t kb = p.q_pos0 + (int64_t)G.tl[0].qb * BM - p.window + 1;
+        if (kb > 0) j0 = (int)(kb / BN);
+        if (j0 > nt - 1) j0 = nt - 1;  // no key left: one fully masked tile (O = 0, LSE = -inf)
+        nt -= j0;
+    }
+    G.nt = nt;
+    G.j0 = j0;
+    return G;
+}
+// the m-th work item of this CTA (-1: none left), from the ring the K~ producer fills; every consumer
+// warp reads each slot once and releases it (one arrive per warp; single-lane roles call with
+// whole_warp = false)
+__device__ __forceinline__ int ring_get(volatile int *ring, uint32_t ifull, uint32_t iempty, int m, bool whole_warp) {
+    const int slot = m & (NRING - 1);
+    mbar_wait(ifull + 8u * slot, (m / NRING) & 1);
+    const int item = ring[slot];
+    if (whole_warp) __syncwarp();
+    if (!whole_warp || (threadIdx.x & 31) == 0) mbar_arrive(iempty + 8u * slot);
+    return item;
+}
+
 #ifdef SFA_TIMELINE
 #define TLREC(tag)                                                                                   \
     do {                                                                                             \
@@ -201,38 +252,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t bar0 = sbase + C::OFF_BAR;
 #define BAR(i) (bar0 + 8u * (uint32_t)(i))
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + C::OFF_BAR + 176);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(gbase + C::OFF_BAR + 232);
+    volatile int *ring = reinterpret_cast<volatile int *>(gbase + C::OFF_BAR + 240);  // NRING item ids
     float *fac = reinterpret_cast<float *>(gbase + C::OFF_F);
 
-    int b;
-    Tile tl[2];
-    decode_item(a, blockIdx.x, b, tl);
-    const int g = tl[0].h / (p.H / p.H_kv);
-    int nt = a.nkt;
-    if (p.causal) {
-        const int qbl = tl[1].valid ? tl[1].qb : tl[0].qb;
-        int64_t last = (int64_t)qbl * BM + BM - 1;
-        if (last > p.n_q - 1) last = p.n_q - 1;
-        const int64_t lim = (p.q_pos0 + last) / BN + 1;
-        if (lim < nt) nt = (int)lim;
-    }
-    // sliding window (N4): key tiles before the window of the CTA's first row are skipped; every loop
-    // below runs over the nt tiles j0, j0 + 1, ... (j relative, key tile j0 + j)
-    int j0r = 0;
-    if (WIN) {
-        const int64_t kb = p.q_pos0 + (int64_t)tl[0].qb * BM - p.window + 1;
-        if (kb > 0) j0r = (int)(kb / BN);
-        if (j0r > nt - 1) j0r = nt - 1;  // no key left: one fully masked tile (O = 0, LSE = -inf)
-        nt -= j0r;
-    }
-    const int j0 = WIN ? j0r : 0;
+#define ITEM_LOOP_BEGIN(WHOLE_WARP)                                                                 \
+    for (int m_ = 0;; ++m_) {                                                                      \
+        const int item_ = ring_get(ring, BAR(IFULL), BAR(IEMPTY), m_, WHOLE_WARP);                 \
+        if (item_ < 0) break;                                                                      \
+        const ItemGeo G_ = item_geo<WIN>(a, item_);                                                \
+        const int b = G_.b, g = G_.g, nt = G_.nt, j0 = G_.j0;                                      \
+        const Tile tl[2] = {G_.tl[0], G_.tl[1]};                                                   \
+        (void)b; (void)g; (void)tl;
+#define ITEM_LOOP_END }
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NBAR; ++i) {
             uint32_t cnt = 1;
-            if ((!SFA_OT_KTMA && (i == KFULL || i == KFULL + 1)) || i == SEMPTY || i == SEMPTY + 1 || i == QFULL) cnt = 4;
+            if (i == SEMPTY || i == SEMPTY + 1 || i == QFULL) cnt = 4;
             if (FUSEQ && i == QFULL) cnt = 8;  // the eight softmax warps build Q~
-            if (i == PFULL || i == PFULL + 1) cnt = 8;
+            if (i == PFULL || i == PFULL + 1 || i == OEMPTY) cnt = 8;
+            if (i >= IEMPTY && i < IEMPTY + NRING) cnt = FUSEQ ? 10 : 14;  // V, MMA, 8 softmax (+ 4 Q~) warps
             mbar_init(BAR(i), cnt);
         }
         fence_mbar_init();
@@ -240,7 +280,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
     if (warp == 12) tmem_alloc<512>(smem_u32(tmem_slot));
     if (warp == 13 && lane == 0) {
         tma_prefetch_desc(&tmap_v);
-        if (SFA_OT_KTMA) tma_prefetch_desc(&tmap_k);
+        tma_prefetch_desc(&tmap_k);
     }
     tc_fence_before();
     __syncthreads();
@@ -256,6 +296,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         const uint32_t tS = tmem + lane_off + (uint32_t)(t * 128);
         // O^T: this thread's TMEM lane is output feature r; tile t's queries are columns [128t, 128t+128)
         const uint32_t tO = tmem + lane_off + (uint32_t)(C::O_COL + t * BM);
+        uint32_t sc = 0;  // S tiles of this query tile consumed so far, over all items (phase of SFULL / PFULL)
+        ITEM_LOOP_BEGIN(true)
         const int64_t i = (int64_t)tl[t].qb * BM + r;
         const bool row_ok = tl[t].valid && i < p.n_q;
         int64_t kend = p.n_kv;
@@ -399,7 +441,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                             (rlo <= 0 ? 0xFFFFFFFFu : (rlo >= 32 ? 0u : ~((1u << rlo) - 1u)));
                 }
             }
-            mbar_wait(BAR(SFULL + t), j & 1);
+            mbar_wait(BAR(SFULL + t), sc & 1);
             if (lane == 0 && wq == 0) TLREC(0x1000 | (t << 10) | (j & 1023));
             tc_fence_after();
             uint32_t s[4][32];
@@ -435,7 +477,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
 #pragma unroll
                 for (int c = 0; c < 32; ++c) mq[q] = fmaxf(mq[q], __uint_as_float(s[q][c]));
             }
-            if (DBG && blockIdx.x == 0 && t == 0 && j == 0) {
+            if (DBG && blockIdx.x == 0 && m_ == 0 && t == 0 && j == 0) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
 #pragma unroll
@@ -488,14 +530,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                 }
                 if (h == 0) {
                     if (lane == 0 && wq == 0) TLREC(0x4000 | (t << 10) | (j & 1023));
-#if SFA_OT_PHALF
-                    // the rescale needs every P.V of tile j-1 complete (its second half is the last)
-                    if (rescale && j > 0) mbar_wait(BAR(PEMPTY + 1), (j & 1) ^ 1);
-#else
-                    // P buffer j % NP free (its last P.V, of P(j - NP), complete)
-                    mbar_wait(BAR(PEMPTY + j % C::NP), ((j / C::NP) & 1) ^ 1);
+                    // the P buffer is free (the previous P.V, over all items, has read it)
+                    mbar_wait(BAR(PEMPTY), (sc & 1) ^ 1);
                     if (lane == 0 && wq == 0) TLREC(0x7000 | (t << 10) | (j & 1023));
-#endif
                     if (rescale && j > 0) {
                         named_bar_sync(bar_id, 128);  // every row's alpha is in f_t
                         tc_fence_after();
@@ -517,35 +554,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                         tmem_st_wait();
                     }
                 }
-#if SFA_OT_PHALF
-                // half h of the P buffer is free once P.V(j-1, h) has read it
-                mbar_wait(BAR(PEMPTY + h), (j & 1) ^ 1);
-                if (h == 0 && lane == 0 && wq == 0) TLREC(0x7000 | (t << 10) | (j & 1023));
-#endif
                 // P row (t*128 + r), atom h: 16-byte chunk c8 swizzled by row
 #pragma unroll
                 for (int c8 = 0; c8 < 8; ++c8)
-                    sts_v4(prow + (uint32_t)(j % C::NP) * C::PT + (uint32_t)h * (2 * BM * 128) + ((uint32_t)(c8 ^ (r & 7)) << 4), pk[4 * c8], pk[4 * c8 + 1],
+                    sts_v4(prow + (uint32_t)h * (2 * BM * 128) + ((uint32_t)(c8 ^ (r & 7)) << 4), pk[4 * c8], pk[4 * c8 + 1],
                            pk[4 * c8 + 2], pk[4 * c8 + 3]);
-#if SFA_OT_PHALF
-                // hand half h to the tensor core now: P.V(j, 0) runs while half 1 is exponentiated
-                fence_proxy_async_smem();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(BAR(PFULL + h));
-#endif
             }
             l += rs0 + rs1;
-#if !SFA_OT_PHALF
             fence_proxy_async_smem();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(BAR(PFULL + j % C::NP));
-#endif
+            if (lane == 0) mbar_arrive(BAR(PFULL));
             if (lane == 0 && wq == 0) TLREC(0x2000 | (t << 10) | (j & 1023));
+            ++sc;
         }
         // ---- epilogue (step 8): O = 2^e (sum_j P'_j V'_j) / l, V' = V 2^-e (vprep.cu)
-        mbar_wait(BAR(OFULL), 0);
+        mbar_wait(BAR(OFULL), m_ & 1);
         tc_fence_after();
         const float inv = l > 0.f ? __uint_as_float((uint32_t)(127 + vprep_head_exp(__ldg(p.v_amax + b * p.H_kv + g))) << 23) / l : 0.f;
         f_t[r] = inv;
@@ -566,6 +590,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                 sts_u16(addr, __bfloat16_as_ushort(__float2bfloat16_rn(v)));
             }
         }
+        // O^T is read out: the next item's first P.V may overwrite it
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(BAR(OEMPTY));
         named_bar_sync(bar_id, 128);
         const int64_t orow = ((int64_t)b * p.H + tl[t].h) * p.n_q + i;
         if (row_ok) {
@@ -574,35 +602,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
             for (int c = 0; c < DV / 8; ++c) dst[c] = lds_v4(so + (uint32_t)r * (DV * 2) + ((uint32_t)(c ^ (r & 15)) << 4));
             p.lse[orow] = l > 0.f ? (m + __log2f(l) - P_SHIFT) * 0.69314718055994530942f : -INFINITY;
         }
+        // both tiles' staging (the dead P buffer, where the other tile's rows interleave) is read before
+        // either tile stores the next item's P
+        named_bar_sync(5, 2 * BM);
+        ITEM_LOOP_END
     } else if (wg == 2) {
         reg_dealloc<64>();
-        // ============================ decompression of Q~ and K~ ============================
+        // ============================ decompression of Q~ (per item) ============================
         const int r = threadIdx.x - 256;
         const int k = p.k;
         const uint16_t *qv = reinterpret_cast<const uint16_t *>(p.q_val);
-        const uint16_t *kv = reinterpret_cast<const uint16_t *>(p.k_val);
         if (!FUSEQ) {
+            ITEM_LOOP_BEGIN(true)
+            if (m_ > 0) mbar_wait(BAR(QEMPTY), (m_ - 1) & 1);  // the previous item's S MMAs are complete
 #pragma unroll
             for (int t = 0; t < 2; ++t) {
                 const int64_t i = (int64_t)tl[t].qb * BM + r;
                 const bool ok = tl[t].valid && i < p.n_q;
-                const int64_t row = ((int64_t)b * p.H + tl[t].h) * p.n_q + i;
+                const int64_t row = ((int64_t)b * p.H + tl[t].h) * p.n_q + (ok ? i : 0);
                 densify_row<D>(sbase + C::OFF_Q + t * C::QT, BM, r, ok, p.q_idx + row * k, qv + row * k, k);
             }
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(BAR(QFULL));
-        }
-        const int64_t kv0 = ((int64_t)b * p.H_kv + g) * p.n_kv;
-        for (int j = 0; j < (SFA_OT_KTMA ? 0 : nt); ++j) {
-            const int s = j % C::NK, u = j / C::NK;
-            mbar_wait(BAR(KEMPTY + s), (u & 1) ^ 1);
-            const int64_t key = (int64_t)(j0 + j) * BN + r;
-            const bool ok = key < p.n_kv;
-            densify_row<D>(sbase + C::OFF_K + s * C::KT, BN, r, ok, p.k_idx + (kv0 + key) * k, kv + (kv0 + key) * k, k);
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(BAR(KFULL + s));
+            ITEM_LOOP_END
         }
     } else {
         reg_dealloc<80>();
@@ -619,102 +642,117 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                                 umma_desc_sw128(pa + (kk >> 2) * (2 * BM * 128) + (kk & 3) * 32, 16, 1024), idO,
                                 (acc || kk > 0) ? 1u : 0u);
                 };
-                auto mma_S = [&](int s) {  // both tiles, instruction by instruction (two accumulators)
-                    const uint32_t ka = sbase + C::OFF_K + s * C::KT;
+                // one stream of key tiles over all items of this CTA: the S of the next tile (of this item,
+                // or the next item's first) is issued before the P.V of the current one
+                uint32_t kc = 0, gs = 0, vc = 0;  // K~ tiles consumed, S tiles issued (per query tile), V tiles
+                auto next_S = [&](bool last_of_item) {
+                    const int s1 = (int)(kc % C::NK);
+                    mbar_wait(BAR(KFULL + s1), (kc / C::NK) & 1);
+                    const uint32_t ka = sbase + C::OFF_K + s1 * C::KT;
 #pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const uint32_t off_q = (kk >> 2) * BM * 128 + (kk & 3) * 32;
-                        const uint32_t off_k = (kk >> 2) * BN * 128 + (kk & 3) * 32;
-                        const uint64_t kd = umma_desc_sw128(ka + off_k, 16, 1024);
-#pragma unroll
-                        for (int t = 0; t < 2; ++t)
-                            umma_ss(tmem + t * 128, umma_desc_sw128(sbase + C::OFF_Q + t * C::QT + off_q, 16, 1024), kd,
-                                    idS, kk > 0);
-                    }
-                };
-                mbar_wait(BAR(QFULL), 0);
-                mbar_wait(BAR(KFULL + 0), 0);
-                tc_fence_after();
-                mma_S(0);
-                umma_commit(BAR(SFULL + 0));
-                umma_commit(BAR(SFULL + 1));
-                umma_commit(BAR(KEMPTY + 0));
-                for (int j = 0; j < nt; ++j) {
-                    if (j + 1 < nt) {
-                        const int s1 = (j + 1) & 1, u1 = (j + 1) >> 1;
-                        mbar_wait(BAR(KFULL + s1), u1 & 1);
-                        const uint32_t ka = sbase + C::OFF_K + s1 * C::KT;
-#pragma unroll
-                        for (int t = 0; t < 2; ++t) {  // each tile's S as soon as that tile has read the last one
-                            mbar_wait(BAR(SEMPTY + t), j & 1);
-                            tc_fence_after();
-#pragma unroll
-                            for (int kk = 0; kk < D / 16; ++kk)
-                                umma_ss(tmem + t * 128,
-                                        umma_desc_sw128(sbase + C::OFF_Q + t * C::QT + (kk >> 2) * BM * 128 + (kk & 3) * 32, 16, 1024),
-                                        umma_desc_sw128(ka + (kk >> 2) * BN * 128 + (kk & 3) * 32, 16, 1024), idS, kk > 0);
-                            umma_commit(BAR(SFULL + t));
-                        }
-                        umma_commit(BAR(KEMPTY + s1));
-                    }
-                    mbar_wait(BAR(VFULL), j & 1);  // NV == 1 here
-#if SFA_OT_PHALF
-                    // O^T += V(j)^T P(j)^T in two 64-key halves, each as soon as both tiles stored it
-                    for (int h = 0; h < 2; ++h) {
-                        mbar_wait(BAR(PFULL + h), j & 1);
-                        if (h == 0) TLREC(0x3000 | (j & 1023));
+                    for (int t = 0; t < 2; ++t) {  // each tile's S as soon as that tile has read its last one
+                        if (gs > 0) mbar_wait(BAR(SEMPTY + t), (gs - 1) & 1);
                         tc_fence_after();
-                        const uint32_t va = sbase + C::OFF_V, pa = sbase + C::OFF_P + h * (2 * BM * 128);
 #pragma unroll
-                        for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
-                            umma_ss(tmem + C::O_COL, umma_desc_sw128(va + kk * 2048, BN * 128, 1024),
-                                    umma_desc_sw128(pa + (kk & 3) * 32, 16, 1024), idO, (j > 0 || kk > 0) ? 1u : 0u);
-                        umma_commit(BAR(PEMPTY + h));
+                        for (int kk = 0; kk < D / 16; ++kk)
+                            umma_ss(tmem + t * 128,
+                                    umma_desc_sw128(sbase + C::OFF_Q + t * C::QT + (kk >> 2) * BM * 128 + (kk & 3) * 32, 16, 1024),
+                                    umma_desc_sw128(ka + (kk >> 2) * BN * 128 + (kk & 3) * 32, 16, 1024), idS, kk > 0);
+                        umma_commit(BAR(SFULL + t));
                     }
-#else
-                    mbar_wait(BAR(PFULL), j & 1);
-                    TLREC(0x3000 | (j & 1023));
-                    tc_fence_after();
-                    mma_O(j > 0, 0, 0);
-                    umma_commit(BAR(PEMPTY));
-#endif
-                    umma_commit(BAR(VEMPTY));
+                    umma_commit(BAR(KEMPTY + s1));
+                    if (last_of_item) umma_commit(BAR(QEMPTY));  // Q~ may be rebuilt for the next item
+                    ++kc;
+                    ++gs;
+                };
+                int m = 0, item = ring_get(ring, BAR(IFULL), BAR(IEMPTY), 0, false);
+                if (item >= 0) {
+                    ItemGeo G = item_geo<WIN>(a, item);
+                    mbar_wait(BAR(QFULL), 0);
+                    next_S(G.nt == 1);
+                    for (;;) {
+                        int item_n = -1;
+                        ItemGeo Gn = G;
+                        for (int j = 0; j < G.nt; ++j) {
+                            if (j + 1 < G.nt) {
+                                next_S(j + 2 == G.nt);
+                            } else {  // the next item's first S overlaps this item's tail.  Read only now:
+                                // the K~ producer publishes the next item after this item's last K~ load
+                                item_n = ring_get(ring, BAR(IFULL), BAR(IEMPTY), m + 1, false);
+                                if (item_n >= 0) {
+                                    Gn = item_geo<WIN>(a, item_n);
+                                    mbar_wait(BAR(QFULL), (m + 1) & 1);
+                                    next_S(Gn.nt == 1);
+                                }
+                            }
+                            mbar_wait(BAR(VFULL), vc & 1);  // one V stage
+                            mbar_wait(BAR(PFULL), vc & 1);  // one P per key tile
+                            TLREC(0x3000 | (j & 1023));
+                            if (j == 0 && m > 0) mbar_wait(BAR(OEMPTY), (m - 1) & 1);  // O^T read out
+                            tc_fence_after();
+                            mma_O(j > 0, 0, 0);
+                            umma_commit(BAR(PEMPTY));
+                            umma_commit(BAR(VEMPTY));
+                            ++vc;
+                        }
+                        umma_commit(BAR(OFULL));
+                        if (item_n < 0) break;
+                        G = Gn;
+                        ++m;
+                    }
                 }
-                umma_commit(BAR(OFULL));
             }
             __syncwarp();
         } else if (warp == 13) {
             // ============================ TMA producer for V ============================
             if (lane == 0) {
+                uint32_t vc = 0;
+                ITEM_LOOP_BEGIN(false)
                 const int bhkv = b * p.H_kv + g;
-                for (int j = 0; j < nt; ++j) {
-                    const int vs = j % C::NV;
-                    mbar_wait(BAR(VEMPTY + vs), ((j / C::NV) & 1) ^ 1);
+                for (int j = 0; j < nt; ++j, ++vc) {
+                    const int vs = (int)(vc % C::NV);
+                    mbar_wait(BAR(VEMPTY + vs), ((vc / C::NV) & 1) ^ 1);
                     mbar_arrive_expect_tx(BAR(VFULL + vs), C::VT);
                     const uint32_t dst = sbase + C::OFF_V + vs * C::VT;
 #pragma unroll
                     for (int cb = 0; cb < DV / 64; ++cb)
                         tma_load_3d(dst + cb * BN * 128, &tmap_v, BAR(VFULL + vs), cb * 64, (j0 + j) * BN, bhkv);
                 }
+                ITEM_LOOP_END
             }
             __syncwarp();
-        } else if (warp == 14 && SFA_OT_KTMA) {
+        } else if (warp == 14) {
             // ============================ TMA producer for K~ (decompressed rows) ============================
             if (lane == 0) {
+                uint32_t kc = 0;
+                for (int m_ = 0;; ++m_) {
+                    // claim the next item and publish it to the other roles
+                    const int slot = m_ & (NRING - 1);
+                    mbar_wait(BAR(IEMPTY + slot), ((m_ / NRING) & 1) ^ 1);
+                    int item_ = m_ == 0 ? (int)blockIdx.x : (int)atomicAdd(p.sched, 1u) + (int)gridDim.x;
+                    if (item_ >= a.items) item_ = -1;
+                    ring[slot] = item_;
+                    mbar_arrive(BAR(IFULL + slot));
+                    if (item_ < 0) break;
+                    const ItemGeo G_ = item_geo<WIN>(a, item_);
+                    const int b = G_.b, g = G_.g, nt = G_.nt, j0 = G_.j0;
                 const int bhkv = b * p.H_kv + g;
-                for (int j = 0; j < nt; ++j) {
-                    const int s = j % C::NK, u = j / C::NK;
-                    mbar_wait(BAR(KEMPTY + s), (u & 1) ^ 1);
+                for (int j = 0; j < nt; ++j, ++kc) {
+                    const int s = (int)(kc % C::NK);
+                    mbar_wait(BAR(KEMPTY + s), ((kc / C::NK) & 1) ^ 1);
                     mbar_arrive_expect_tx(BAR(KFULL + s), C::KT);
                     const uint32_t dst = sbase + C::OFF_K + s * C::KT;
 #pragma unroll
                     for (int cb = 0; cb < D / 64; ++cb)
                         tma_load_3d(dst + cb * BN * 128, &tmap_k, BAR(KFULL + s), cb * 64, (j0 + j) * BN, bhkv);
                 }
+                ITEM_LOOP_END
             }
             __syncwarp();
         }
     }
+#undef ITEM_LOOP_BEGIN
+#undef ITEM_LOOP_END
     tc_fence_before();
     __syncthreads();
     if (warp == 12) {
@@ -754,7 +792,7 @@ cudaError_t launch_t(const OtArgs &a, cudaStream_t stream, int items) {
     if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
     CUtensorMap tk;  // K~ rows (bf16 [B*H_kv][n_kv][D]), same box shape and swizzle as the decompression wrote
     memset(&tk, 0, sizeof(tk));
-    if (SFA_OT_KTMA) {
+    {
         if (p.k_dense == nullptr) return cudaErrorInvalidValue;
         cuuint64_t kdims[3] = {(cuuint64_t)D, (cuuint64_t)p.n_kv, (cuuint64_t)p.B * p.H_kv};
         cuuint64_t kstrides[2] = {(cuuint64_t)D * 2, (cuuint64_t)p.n_kv * D * 2};
@@ -774,7 +812,19 @@ cudaError_t launch_t(const OtArgs &a, cudaStream_t stream, int items) {
                                                    : attn_sm100_ot_kernel<D, false, false, false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
-    kern<<<items, NTHREADS, C::SMEM, stream>>>(tm, tk, a);
+    // persistent: one CTA per SM takes items from the work counter; the fused-Q prologue keeps one item
+    // per CTA (grid = items: every CTA's second claim is past the end)
+    if (p.sched == nullptr) return cudaErrorInvalidValue;
+    cudaError_t me = cudaMemsetAsync(p.sched, 0, sizeof(uint32_t), stream);
+    if (me != cudaSuccess) return me;
+    int grid = items;
+    if (p.q_dense == nullptr && !SFA_OT_ONE_ITEM_PER_CTA) {
+        int sms = 148, dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (grid > sms) grid = sms;
+    }
+    kern<<<grid, NTHREADS, C::SMEM, stream>>>(tm, tk, a);
     return cudaGetLastError();
 }
 
@@ -803,6 +853,7 @@ cudaError_t launch_attn_sm100_ot(const AttnParams &p, int d, int d_v, cudaStream
     }
     if (items == 0) return cudaSuccess;
     if (items > INT32_MAX) return cudaErrorNotSupported;
+    a.items = (int)items;
     return d == 64 ? launch_t<64>(a, stream, (int)items) : launch_t<128>(a, stream, (int)items);
 }
 

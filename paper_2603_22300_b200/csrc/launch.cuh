@@ -13,6 +13,7 @@ struct AttnParams {
     const void *v16;         // sm100: fp16 copy of V scaled by 2^-e per (b, kv head) (vprep.cu)
     const uint32_t *v_amax;  // sm100: per (b, kv head) max|V| bits, e = vprep_head_exp(bits)
     const void *k_dense = nullptr;  // SM100_OT: decompressed K~ rows, bf16 [B][H_kv][n_kv][d] (vprep.cu)
+    uint32_t *sched = nullptr;      // SM100_OT: the persistent tile scheduler's work counter (workspace)
     void *o;
     float *lse;
     const uint8_t *ws;
@@ -39,6 +40,9 @@ cudaError_t launch_kfmask(const uint8_t *k_idx, int64_t bh_kv, int64_t n_kv, int
 
 cudaError_t launch_topk(const void *x, bool bf16, int64_t rows, int d, int64_t ld, int k, uint8_t *idx, void *val,
                         uint32_t *status_word, cudaStream_t stream);
+cudaError_t launch_topk_pair(const void *x0, int64_t rows0, int64_t ld0, uint8_t *idx0, void *val0, const void *x1,
+                             int64_t rows1, int64_t ld1, uint8_t *idx1, void *val1, int d, int k,
+                             uint32_t *status_word, cudaStream_t stream);
 cudaError_t launch_bucket(const uint8_t *k_idx, const void *k_val, bool bf16, int d, int k, int64_t bh_kv,
                           int64_t n_kv, const BucketLayout &L, void *ws, cudaStream_t stream);
 // P.V operand prep for the sm100 kernel: amax[bh] = max|V| bits, v16 = fp16(V * 2^-e) (vprep.cu)

@@ -59,6 +59,7 @@ def lib() -> ctypes.CDLL:
         sig = {
             "sfa_status_string": ([I32], ctypes.c_char_p),
             "sfa_topk_codes": ([P, I32, I64, I32, I64, I32, P, P, P, P], I32),
+            "sfa_topk_codes_qk": ([P, I64, I64, P, P, P, I64, I64, P, P, I32, I32, I32, P, P], I32),
             "sfa_attn_workspace_bytes": ([D], SZ),
             "sfa_attn_fwd": ([D, P, P, P, P, P, P, P, P, SZ, P], I32),
             "sfa_bucket_keys": ([D, P, P, P, SZ, P], I32),
@@ -93,7 +94,7 @@ def lib() -> ctypes.CDLL:
     return _lib
 
 
-EXPORTS = ("sfa_status_string", "sfa_topk_codes", "sfa_attn_workspace_bytes", "sfa_attn_fwd", "sfa_bucket_keys",
+EXPORTS = ("sfa_status_string", "sfa_topk_codes", "sfa_topk_codes_qk", "sfa_attn_workspace_bytes", "sfa_attn_fwd", "sfa_bucket_keys",
            "sfa_attn_fwd_bucketed", "sfa_key_tile", "sfa_forward_scratch_bytes", "sfa_forward",
            "sfa_forward_host", "sfa_device_supported", "sfa_gen_fill", "sfa_debug_sm100_scores",
            "sfa_attn_prepare", "sfa_attn_fwd_prepared", "sfa_dist_unique_id", "sfa_dist_init", "sfa_dist_destroy",
@@ -189,6 +190,23 @@ def topk_codes(x: torch.Tensor, k: int, status: torch.Tensor | None = None):
     _check(lib().sfa_topk_codes(_p(x), _dt(x), rows, d, d, k, _p(idx), _p(val), _p(status), _stream()),
            "sfa_topk_codes")
     return idx, val
+
+
+def topk_codes_qk(q: torch.Tensor, kx: torch.Tensor, k: int, status: torch.Tensor | None = None):
+    """Stage 1 on Q and on K in one launch (sfa_topk_codes_qk): the same codes as two topk_codes calls."""
+    _dev(q)
+    _dev(kx)
+    if q.dtype != kx.dtype or q.shape[-1] != kx.shape[-1] or not q.is_contiguous() or not kx.is_contiguous():
+        raise ValueError("topk_codes_qk: q and k need the same dtype and d, contiguous")
+    d = q.shape[-1]
+    out = []
+    for x in (q, kx):
+        out.append((torch.empty(x.shape[:-1] + (k,), dtype=torch.uint8, device=x.device),
+                    torch.empty(x.shape[:-1] + (k,), dtype=x.dtype, device=x.device)))
+    (qi, qv), (ki, kv) = out
+    _check(lib().sfa_topk_codes_qk(_p(q), q.numel() // d, d, _p(qi), _p(qv), _p(kx), kx.numel() // d, d, _p(ki),
+                                   _p(kv), _dt(q), d, k, _p(status), _stream()), "sfa_topk_codes_qk")
+    return qi, qv, ki, kv
 
 
 def _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, kernel, dtype, edges_only=False, window=0):

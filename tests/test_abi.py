@@ -50,6 +50,13 @@ def test_host_validation_before_launch(sfa):
     assert L.sfa_topk_codes(dummy, 7, 10, 128, 128, 8, dummy, dummy, None, None) == 1
     assert L.sfa_topk_codes(None, 1, 10, 128, 128, 8, dummy, dummy, None, None) == 1
     assert L.sfa_topk_codes(dummy, 1, 0, 128, 128, 8, None, None, None, None) == 0  # empty is ok
+    # the fused Q + K launch validates both tensors before any launch
+    qk = L.sfa_topk_codes_qk
+    assert qk(dummy, 10, 128, dummy, dummy, dummy, 10, 128, dummy, dummy, 1, 128, 0, None, None) == 1   # k = 0
+    assert qk(dummy, 10, 128, dummy, dummy, dummy, 10, 64, dummy, dummy, 1, 128, 8, None, None) == 1   # K ld < d
+    assert qk(dummy, 10, 128, dummy, dummy, None, 10, 128, dummy, dummy, 1, 128, 8, None, None) == 1   # K null
+    assert qk(dummy, 10, 96, dummy, dummy, dummy, 10, 96, dummy, dummy, 1, 96, 8, None, None) == 3     # d = 96
+    assert qk(dummy, 0, 128, None, None, dummy, 0, 128, None, None, 1, 128, 8, None, None) == 0      # empty
 
 
 def desc(sfa, **kw):
@@ -63,10 +70,12 @@ def test_desc_validation(sfa):
     ok = desc(sfa, kernel=sfa.KERNEL_SIMT)
     assert L.sfa_attn_workspace_bytes(ctypes.byref(ok)) > 0
     # the default sm_100a kernel (SM100_OT, no buckets): the 256-aligned max|V| per (b, kv head) + the
-    # fp16 copy of V (reading A12), then 256-aligned, the decompressed bf16 K~ rows its TMA reads
+    # fp16 copy of V (reading A12), then 256-aligned, the decompressed bf16 K~ rows its TMA reads, then
+    # 256 bytes for the persistent tile scheduler's work counter
     v16 = 256 + 1 * 2 * 300 * 128 * 2
     kd = 1 * 2 * 300 * 128 * 2
-    assert L.sfa_attn_workspace_bytes(ctypes.byref(desc(sfa))) == (v16 + 255) // 256 * 256 + (kd + 255) // 256 * 256
+    assert L.sfa_attn_workspace_bytes(ctypes.byref(desc(sfa))) == \
+        (v16 + 255) // 256 * 256 + (kd + 255) // 256 * 256 + 256
     # SM100 (d_v = 64 default) decompresses the key codes on chip: V prep only
     assert L.sfa_attn_workspace_bytes(ctypes.byref(desc(sfa, kernel=sfa.KERNEL_SM100))) == v16
     bad = [dict(H=3, H_kv=2), dict(k=0), dict(k=129), dict(n_q=0), dict(n_kv=0), dict(scale=-1.0),

@@ -104,3 +104,19 @@ def test_qwen3_q_codes_all_rows(lib):
     oi, ov = oracle_codes(q_host, 16)
     np.testing.assert_array_equal(from_torch(gi), oi)
     np.testing.assert_array_equal(from_torch(gv), ov)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("d,kk", [(64, 8), (128, 16), (128, 4), (128, 127), (128, 128)])
+def test_qk_pair_launch_equals_oracle(lib, dtype, d, kk):
+    """sfa_topk_codes_qk (Q and K rows in ONE launch, segment per tensor) gives the oracle's codes for
+    both tensors, including ragged row counts that end mid-CTA in either segment."""
+    q = inputs.gen(77 + d, inputs.TID_Q, (1, 3, 301, d), dtype)
+    kx = inputs.gen(77 + d, inputs.TID_K, (1, 1, 173, d), dtype, variant="lattice")
+    qi, qv, ki, kv = lib.topk_codes_qk(to_torch(q, dtype), to_torch(kx, dtype), kk)
+    import torch
+    torch.cuda.synchronize()
+    for (gi, gv), x in (((qi, qv), q), ((ki, kv), kx)):
+        oi, ov = oracle_codes(x, kk)
+        np.testing.assert_array_equal(from_torch(gi), oi)
+        np.testing.assert_array_equal(from_torch(gv), ov)
