@@ -302,6 +302,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         const bool row_ok = tl[t].valid && i < p.n_q;
         int64_t kend = p.n_kv;
         if (p.causal && p.q_pos0 + i + 1 < kend) kend = p.q_pos0 + i + 1;
+#ifdef SFA_FAULT_CAUSAL_PLUS1  // negative control: the diagonal's next key also allowed
+        if (p.causal && kend < p.n_kv) kend += 1;
+#endif
         const int64_t kbeg = WIN ? p.q_pos0 + i - p.window + 1 : 0;  // N4 sliding window
         const float cs = a.c_scale;
         if (FUSEQ) {
@@ -499,6 +502,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
             const float m_new = fmaxf(m, mx);
             // O^T columns are shared by the whole warpgroup: rescale all of tile t or none of it
             const bool rescale = named_bar_or(bar_id, 128, m_new > m + 8.f);
+#ifdef SFA_FAULT_NO_O_RESCALE  // negative control: alpha applied to l but never to O^T
+            const bool rescale_o = false;
+#else
+            const bool rescale_o = rescale;
+#endif
             if (lane == 0 && wq == 0) TLREC(0x6000 | (t << 10) | (j & 1023));
             if (rescale) {
                 const float alpha = (m_new == -INFINITY) ? 1.f : fast_exp2(m - m_new);
@@ -533,7 +541,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                     // the P buffer is free (the previous P.V, over all items, has read it)
                     mbar_wait(BAR(PEMPTY), (sc & 1) ^ 1);
                     if (lane == 0 && wq == 0) TLREC(0x7000 | (t << 10) | (j & 1023));
-                    if (rescale && j > 0) {
+                    if (rescale_o && j > 0) {
                         named_bar_sync(bar_id, 128);  // every row's alpha is in f_t
                         tc_fence_after();
 #pragma unroll 1
@@ -840,6 +848,9 @@ cudaError_t launch_attn_sm100_ot(const AttnParams &p, int d, int d_v, cudaStream
     a.nqb = (int)((p.n_q + BM - 1) / BM);
     a.nkt = (int)((p.n_kv + BN - 1) / BN);
     a.c_scale = p.scale_log2;
+#ifdef SFA_FAULT_SCALE  // negative control: logit scale off by 2^-9 relative
+    a.c_scale *= 1.f + 1.f / 512.f;
+#endif
     a.dbg = dbg;
     const int R = p.H / p.H_kv;
     a.pair_heads = (R % 2 == 0) ? 1 : 0;

@@ -76,6 +76,7 @@ __device__ __forceinline__ void select_masks(const uint32_t (&ab)[NW], int k, ui
     int need = k;
 #pragma unroll
     for (int w = 0; w < NM; ++w) need -= __popc(gm[w]);
+#ifndef SFA_FAULT_TOPK_TIE_HIGH
 #pragma unroll
     for (int w = 0; w < NM; ++w)
         while (need > 0 && em[w] != 0u) {  // lowest-index ties first (A2)
@@ -83,6 +84,16 @@ __device__ __forceinline__ void select_masks(const uint32_t (&ab)[NW], int k, ui
             em[w] &= em[w] - 1u;
             --need;
         }
+#else  // negative control (tools/gpu_mutants.sh): ties taken from the highest index
+#pragma unroll
+    for (int w = NM - 1; w >= 0; --w)
+        while (need > 0 && em[w] != 0u) {
+            const uint32_t hb = 0x80000000u >> __clz(em[w]);
+            gm[w] |= hb;
+            em[w] &= ~hb;
+            --need;
+        }
+#endif
 }
 
 }  // namespace tk

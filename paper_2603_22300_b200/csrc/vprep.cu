@@ -42,7 +42,11 @@ __global__ void __launch_bounds__(256) v_to_f16_kernel(const uint4 *__restrict__
                                                         uint2 *__restrict__ out) {
     for (int64_t bh = blockIdx.y; bh < n_bh; bh += gridDim.y) {
     const int e = vprep_head_exp(__ldg(amax + bh));
+#ifndef SFA_FAULT_VSCALE
     const float sc = __uint_as_float((uint32_t)(127 - e) << 23);  // 2^-e, exact
+#else  // negative control: V' = V 2^(1-e) while the epilogue multiplies by 2^e
+    const float sc = __uint_as_float((uint32_t)(128 - e) << 23);
+#endif
     const uint4 *src = v + (int64_t)bh * vec_per_head;
     uint4 *dst = reinterpret_cast<uint4 *>(out) + (int64_t)bh * vec_per_head;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < vec_per_head;
@@ -87,8 +91,12 @@ __global__ void __launch_bounds__(KD_ROWS) k_dense_kernel(const uint8_t *__restr
                 const uint4 vv = __ldg(reinterpret_cast<const uint4 *>(vr + e0));
                 const uint32_t iw[2] = {ii.x, ii.y}, vw[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
-                for (int e = 0; e < 8; ++e)
+                for (int e = 0; e < 8; ++e) {
+#ifdef SFA_FAULT_KDENSE_DROP_LAST  // negative control: the row's last selected feature left at 0
+                    if (e0 + e == k - 1) continue;
+#endif
                     row[(iw[e >> 2] >> (8 * (e & 3))) & 0xFFu] = (uint16_t)(vw[e >> 1] >> (16 * (e & 1)));
+                }
             }
         } else {
             for (int e = 0; e < k; ++e) row[__ldg(ir + e)] = __ldg(vr + e);
