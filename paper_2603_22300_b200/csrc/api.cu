@@ -400,16 +400,22 @@ static sfa_status forward_impl(const sfa_attn_desc *desc, const void *q, const v
     const Scratch L = scratch_layout(desc);
     const bool bf16 = desc->dtype == SFA_BF16;
     cudaError_t e;
-    // step 1 on Q as its own kernel: measured faster than the fused prologue (N3(ii))
+    // step 1 on Q as its own kernel (measured faster than the fused prologue, N3(ii)), Q and K
+    // rows in one launch when both take the bf16 row kernel
     const bool fuse = false;
-    if (!fuse) {
+    if (bf16 && desc->k < desc->d) {
+        e = launch_topk_pair(q, (int64_t)desc->B * desc->H * desc->n_q, desc->d, S + L.q_idx, S + L.q_val, k,
+                             (int64_t)desc->B * desc->H_kv * desc->n_kv, desc->d, S + L.k_idx, S + L.k_val, desc->d,
+                             desc->k, status, st);
+        if (e != cudaSuccess) return SFA_ERR_CUDA;
+    } else {
         e = launch_topk(q, bf16, (int64_t)desc->B * desc->H * desc->n_q, desc->d, desc->d, desc->k, S + L.q_idx,
                         S + L.q_val, status, st);
         if (e != cudaSuccess) return SFA_ERR_CUDA;
+        e = launch_topk(k, bf16, (int64_t)desc->B * desc->H_kv * desc->n_kv, desc->d, desc->d, desc->k, S + L.k_idx,
+                        S + L.k_val, status, st);
+        if (e != cudaSuccess) return SFA_ERR_CUDA;
     }
-    e = launch_topk(k, bf16, (int64_t)desc->B * desc->H_kv * desc->n_kv, desc->d, desc->d, desc->k, S + L.k_idx,
-                    S + L.k_val, status, st);
-    if (e != cudaSuccess) return SFA_ERR_CUDA;
     if (!fuse || !fusable(desc))
         return run_attn(desc, S + L.q_idx, S + L.q_val, S + L.k_idx, S + L.k_val, v, o, lse, S + L.ws, st);
     sfa_status s = run_prepare(desc, S + L.k_idx, S + L.k_val, v, S + L.ws, st);
