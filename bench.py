@@ -882,7 +882,7 @@ def main():
                 "frac": achieved / mufu_peak, "traffic": traffic,
                 "traffic_unit": "DRAM bytes per launch (ncu --set full capture, profiles/ncu_traffic.json); "
                                 f"algorithmic minimum {W.attn_min_bytes()} B",
-                "peak_source": f"148 SMs x 16 ex2/clk x {pk['sm_max_mhz']:.0f} MHz (DESIGN.md 'Rooflines')",
+                "peak_source": f"148 SMs x 16 ex2/clk (measured, profiles/r02_mufu_bench.txt) x {pk['sm_max_mhz']:.0f} MHz",
                 "other_floors": {
                     # tensor pipe: S = Q~K~^T (2d) + P.V (2 d_v) FLOPs per allowed pair, vs the measured bf16 peak
                     "tensor_frac": (2.0 * (d + d_v) * pairs / (attn_ms / 1e3)) / (pk["bf16_tflops"] * 1e12)
