@@ -48,6 +48,12 @@ __device__ __forceinline__ void issue8(uint32_t tmem, uint32_t A, uint32_t B, ui
             constexpr uint32_t id = umma_idesc_f16kind(128, N, 0, 0, 1);
             if (ELECT) umma_ss_elect(tmem, ad, bd, id, kk > 0);
             else umma_ss(tmem, ad, bd, id, kk > 0);
+        } else if (MODE == 4 || MODE == 5) {  // TS S with A (Q~) in TMEM, N = 64 / 128 (B = K~, K-major)
+            constexpr int N = MODE == 4 ? 64 : 128;
+            const uint64_t bd = umma_desc_sw128(B + (kk >> 2) * (N * 128) + (kk & 3) * 32, 16, 1024);
+            constexpr uint32_t id = umma_idesc_f16kind(128, N, 0, 0, 1);
+            if (ELECT) umma_ts_elect(tmem + 256, tmem + 128 + kk * 8, bd, id, kk > 0);
+            else umma_ts(tmem + 256, tmem + 128 + kk * 8, bd, id, kk > 0);
         } else {  // TS P.V, N = 128
             const uint64_t bd = umma_desc_sw128(V + kk * 2048, 16384, 1024);
             constexpr uint32_t id = umma_idesc_f16kind(128, 128, 0, 1, 0);
@@ -135,5 +141,8 @@ int main() {
     run<2, true>("SS M128 N256 K16 bf16", 128);
     run<3, false>("TS M128 N128 K16 fp16 (P.V, A in TMEM)", 64);
     run<3, true>("TS M128 N128 K16 fp16 (P.V, A in TMEM)", 64);
+    run<4, false>("TS M128 N64  K16 bf16 (S, A = Q~ in TMEM)", 32);
+    run<4, true>("TS M128 N64  K16 bf16 (S, A = Q~ in TMEM)", 32);
+    run<5, true>("TS M128 N128 K16 bf16 (S, A = Q~ in TMEM)", 64);
     return 0;
 }
