@@ -68,9 +68,12 @@ typedef enum {
                                   it for such shapes.                                                      */
     SFA_KERNEL_SM100_OT = 6,   /* SM100 with a transposed output accumulator: O^T += V^T P^T as N = 256 MMAs
                                   over both query tiles, P in shared memory (bf16, d_v = 128)              */
-    SFA_KERNEL_SM100_PP = 7    /* two query tiles in ping-pong: K~ tiles by TMA from key rows decompressed
+    SFA_KERNEL_SM100_PP = 7,   /* two query tiles in ping-pong: K~ tiles by TMA from key rows decompressed
                                   once per key (prepare step), P in TMEM (TS-MMA P.V), exponential phases
                                   of the two softmax warpgroups alternating (bf16, R1, no window)          */
+    SFA_KERNEL_SM100_OTH = 8   /* SM100_OT with Q~ in TMEM (TS-MMA scores over 64-key halves, P handed over
+                                  per half): fewer shared-memory bytes per key (bf16, d_v = 128, R1, no
+                                  window)                                                                */
 } sfa_kernel;
 
 SFA_API const char *sfa_status_string(sfa_status s);

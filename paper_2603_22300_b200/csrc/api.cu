@@ -28,14 +28,16 @@ sfa_status validate_desc(const sfa_attn_desc *d) {
     if (d->causal != 0 && d->causal != 1) return SFA_ERR_INVALID_ARGUMENT;
     if (!(d->scale > 0.f) || !isfinite(d->scale)) return SFA_ERR_INVALID_ARGUMENT;
     if (d->dtype != SFA_F32 && d->dtype != SFA_BF16) return SFA_ERR_INVALID_ARGUMENT;
-    if (d->kernel < SFA_KERNEL_AUTO || d->kernel > SFA_KERNEL_SM100_PP) return SFA_ERR_INVALID_ARGUMENT;
+    if (d->kernel < SFA_KERNEL_AUTO || d->kernel > SFA_KERNEL_SM100_OTH) return SFA_ERR_INVALID_ARGUMENT;
     if (d->d != 64 && d->d != 128) return SFA_ERR_UNSUPPORTED;
     if (d->d_v != 64 && d->d_v != 128) return SFA_ERR_UNSUPPORTED;
     if ((d->kernel == SFA_KERNEL_SM100 || d->kernel == SFA_KERNEL_SM100_PAIR || d->kernel == SFA_KERNEL_SM100_WIDE ||
-         d->kernel == SFA_KERNEL_SM100_OT || d->kernel == SFA_KERNEL_SM100_PP) &&
+         d->kernel == SFA_KERNEL_SM100_OT || d->kernel == SFA_KERNEL_SM100_PP || d->kernel == SFA_KERNEL_SM100_OTH) &&
         d->dtype != SFA_BF16)
         return SFA_ERR_UNSUPPORTED;
-    if ((d->kernel == SFA_KERNEL_SM100_PAIR || d->kernel == SFA_KERNEL_SM100_OT) && d->d_v != 128) return SFA_ERR_UNSUPPORTED;
+    if ((d->kernel == SFA_KERNEL_SM100_PAIR || d->kernel == SFA_KERNEL_SM100_OT || d->kernel == SFA_KERNEL_SM100_OTH) &&
+        d->d_v != 128)
+        return SFA_ERR_UNSUPPORTED;
     if (d->kernel == SFA_KERNEL_DECODE &&
         (d->dtype != SFA_BF16 || (int64_t)(d->H / d->H_kv) * d->n_q > 16))
         return SFA_ERR_UNSUPPORTED;
@@ -87,7 +89,7 @@ size_t vprep_bytes(const sfa_attn_desc *d) {
 // the key-tile feature bitsets (edges.cu)
 bool uses_kdense(const sfa_attn_desc *d) {
     const int k = resolve_kernel(d);
-    return k == SFA_KERNEL_SM100_OT || k == SFA_KERNEL_SM100_PP;
+    return k == SFA_KERNEL_SM100_OT || k == SFA_KERNEL_SM100_PP || k == SFA_KERNEL_SM100_OTH;
 }
 size_t kdense_off(const sfa_attn_desc *d) { return align_up(vprep_bytes(d), 256); }
 size_t kdense_bytes(const sfa_attn_desc *d) {
@@ -180,6 +182,7 @@ sfa_status run_attn_prepared(const sfa_attn_desc *d, const uint8_t *q_idx, const
     if (kern == SFA_KERNEL_SM100_WIDE) return from_launch(launch_attn_sm100_wide(p, d->d, d->d_v, st, dbg));
     if (kern == SFA_KERNEL_SM100_OT) return from_launch(launch_attn_sm100_ot(p, d->d, d->d_v, st, dbg));
     if (kern == SFA_KERNEL_SM100_PP) return from_launch(launch_attn_sm100_pp(p, d->d, d->d_v, st, dbg));
+    if (kern == SFA_KERNEL_SM100_OTH) return from_launch(launch_attn_sm100_oth(p, d->d, d->d_v, st, dbg));
     if (kern == SFA_KERNEL_SM100) return from_launch(launch_attn_sm100(p, d->d, d->d_v, st, dbg));
     return from_cuda(launch_attn_simt(p, d->dtype == SFA_BF16, d->d, d->d_v, st));
 }

@@ -75,6 +75,8 @@ cudaError_t launch_attn_sm100_wide(const AttnParams &p, int d, int d_v, cudaStre
 cudaError_t launch_attn_sm100_ot(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
 // two query tiles in ping-pong, K~ by TMA from p.k_dense, P in TMEM (attn_sm100_pp.cu); R1, no window
 cudaError_t launch_attn_sm100_pp(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
+// SM100_OT with Q~ in TMEM and 64-key score halves (attn_sm100_oth.cu); R1, no window, d_v = 128
+cudaError_t launch_attn_sm100_oth(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
 // backward with the straight-through rule (bwd.cu): D = rowsum(dO . O) into Dws [B*H*n_q], then the
 // dK~/dV and dQ~ tensor-core kernels; gradients w.r.t. the code values and V, fp32
 cudaError_t launch_attn_bwd(const AttnParams &p, int d, int d_v, const void *dO, float *Dws, float *dq, float *dk,

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(_HERE, "libsfa.so")
 
 SFA_F32, SFA_BF16 = 0, 1
 (KERNEL_AUTO, KERNEL_SIMT, KERNEL_SM100, KERNEL_SM100_PAIR, KERNEL_SM100_WIDE, KERNEL_DECODE, KERNEL_SM100_OT,
- KERNEL_SM100_PP) = range(8)
+ KERNEL_SM100_PP, KERNEL_SM100_OTH) = range(9)
 GEN_IID, GEN_LATTICE, GEN_SKEWED = 0, 1, 2
 _STATUS = {0: "ok", 1: "invalid-argument", 2: "invalid-input", 3: "unsupported", 4: "resource-limit",
            5: "cuda-error"}

@@ -83,12 +83,12 @@ def test_peaked_rows_trigger_rescale(lib):
 # ---------------------------------------------------------------------------------------------
 # M = 256 CTA-pair kernel (attn_sm100_pair.cu): same checks
 # ---------------------------------------------------------------------------------------------
-VARIANTS = ["pair", "wide", "ot", "pp"]  # SFA_KERNEL_SM100_PAIR / _WIDE / _OT / _PP
+VARIANTS = ["pair", "wide", "ot", "pp", "oth"]  # SFA_KERNEL_SM100_PAIR / _WIDE / _OT / _PP / _OTH
 
 
 def _kern(lib, name):
     return {"pair": lib.KERNEL_SM100_PAIR, "wide": lib.KERNEL_SM100_WIDE, "ot": lib.KERNEL_SM100_OT,
-            "pp": lib.KERNEL_SM100_PP}[name]
+            "pp": lib.KERNEL_SM100_PP, "oth": lib.KERNEL_SM100_OTH}[name]
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
@@ -121,7 +121,7 @@ def test_variant_score_tile_is_exact_overlap_sum(lib, variant, d, k):
 def test_variant_against_oracle(lib, variant, shape, causal):
     import torch
     B, H, H_kv, n, d, d_v, k = shape
-    if variant in ("pair", "ot") and d_v != 128:
+    if variant in ("pair", "ot", "oth") and d_v != 128:
         pytest.skip("pair / ot kernels need d_v = 128 (M of the transposed product / split over the pair)")
     q, kx, v = host_qkv(56, B, H, H_kv, n, d, d_v, "bf16")
     qi, qv = oracle_codes(q, k)

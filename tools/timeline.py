@@ -14,7 +14,7 @@ from paper_2603_22300_b200 import inputs, sfa  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 kern = {"sm100": sfa.KERNEL_SM100, "pair": sfa.KERNEL_SM100_PAIR, "wide": sfa.KERNEL_SM100_WIDE, "ot": sfa.KERNEL_SM100_OT,
-        "pp": sfa.KERNEL_SM100_PP}[sys.argv[2] if len(sys.argv) > 2 else "sm100"]
+        "pp": sfa.KERNEL_SM100_PP, "oth": sfa.KERNEL_SM100_OTH}[sys.argv[2] if len(sys.argv) > 2 else "sm100"]
 qwen = len(sys.argv) > 3 and sys.argv[3] == "qwen"  # bench config: causal, H=32, H_kv=8 (item 0 = last q block)
 B, H, H_kv, d, d_v, k = (1, 32, 8, 128, 128, 16) if qwen else (1, 2, 1, 128, 128, 16)
 dev = "cuda"
@@ -39,6 +39,17 @@ for tg, c in zip(tag, clk):
     kind, t, u = tg >> 12, (tg >> 10) & 3, tg & 1023
     ev[(names[kind], t, u)] = c
 nu = max(u for (_, _, u) in ev) + 1
+if len(sys.argv) > 2 and sys.argv[2] == "oth":  # 64-key halves u: S ready, max/bar done, P computed, P slot free, P stored, MMA saw P
+    print(f"{cnt} records, {nu} score halves; clocks relative to the first record")
+    print("  u | tile 0: Srdy   bar  exps  Pfree  Pst | tile 1: Srdy   bar  exps  Pfree  Pst | mmaP | period")
+    prev = None
+    for u in range(nu):
+        r = [[ev.get((nm, t, u), -1) for nm in ("S_ready", "max", "max_done", "pempty", "P_stored")] for t in (0, 1)]
+        mp = ev.get(("mma_sawP", 0, u), -1)
+        per = r[0][0] - prev if prev is not None else 0
+        prev = r[0][0]
+        print(f"{u:3d} | " + " ".join(f"{x:6d}" for x in r[0]) + " | " + " ".join(f"{x:6d}" for x in r[1]) + f" | {mp:6d} | {per}")
+    sys.exit(0)
 if len(sys.argv) > 2 and sys.argv[2] == "pp":  # ping-pong kernel: S ready, max done, turn, P stored, MMA saw P
     print(f"{cnt} records, {nu} key tiles; clocks relative to the first record")
     print("  j | tile 0: Srdy  maxd  turn  Pst   mmaP  | tile 1: Srdy  maxd  turn  Pst   mmaP  | exp0  exp1 | period")
