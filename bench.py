@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="qwen3", choices=sorted(accounting.CONFIGS))
-    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "sm100", "pair", "wide", "ot", "pp", "oth"])
+    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "sm100", "ot", "pp", "oth"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--window", type=int, default=0,
                     help="causal sliding window (N4: SFA composed with token sparsity); 0 = full causal")
@@ -621,7 +621,6 @@ def main():
     if world > 1:
         init_group(world, rank, local)
     kernel = {"auto": sfa.KERNEL_AUTO, "simt": sfa.KERNEL_SIMT, "sm100": sfa.KERNEL_SM100,
-              "pair": sfa.KERNEL_SM100_PAIR, "wide": sfa.KERNEL_SM100_WIDE,
               "ot": sfa.KERNEL_SM100_OT, "pp": sfa.KERNEL_SM100_PP, "oth": sfa.KERNEL_SM100_OTH}[args.kernel]
     dt = torch.bfloat16 if W.dtype == "bf16" else torch.float32
     seed = accounting.SEEDS[args.config]
@@ -874,8 +873,6 @@ def main():
     sm100 = W.dtype == "bf16" and args.kernel != "simt"
     kname = {"auto": "attn_sm100_ot_kernel" if d_v == 128 else "attn_sm100_kernel", "sm100": "attn_sm100_kernel",
              "ot": "attn_sm100_ot_kernel", "pp": "attn_sm100_pp_kernel", "oth": "attn_sm100_oth_kernel",
-             "pair": "attn_sm100_pair_kernel",
-             "wide": "attn_sm100_wide_kernel",
              "simt": "attn_simt_kernel"}[args.kernel if sm100 else "simt"]
     roofline = {"bound": "alu", "kernel": kname + (" (step 1 on Q fused + steps 4-8)" if fused_q else " (steps 4-8)"),
                 "achieved": achieved / 1e9, "peak": mufu_peak / 1e9,

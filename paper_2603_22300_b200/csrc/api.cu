@@ -29,6 +29,7 @@ sfa_status validate_desc(const sfa_attn_desc *d) {
     if (!(d->scale > 0.f) || !isfinite(d->scale)) return SFA_ERR_INVALID_ARGUMENT;
     if (d->dtype != SFA_F32 && d->dtype != SFA_BF16) return SFA_ERR_INVALID_ARGUMENT;
     if (d->kernel < SFA_KERNEL_AUTO || d->kernel > SFA_KERNEL_SM100_OTH) return SFA_ERR_INVALID_ARGUMENT;
+    if (d->kernel == SFA_KERNEL_SM100_PAIR || d->kernel == SFA_KERNEL_SM100_WIDE) return SFA_ERR_UNSUPPORTED;  // removed
     if (d->d != 64 && d->d != 128) return SFA_ERR_UNSUPPORTED;
     if (d->d_v != 64 && d->d_v != 128) return SFA_ERR_UNSUPPORTED;
     if ((d->kernel == SFA_KERNEL_SM100 || d->kernel == SFA_KERNEL_SM100_PAIR || d->kernel == SFA_KERNEL_SM100_WIDE ||
@@ -178,8 +179,6 @@ sfa_status run_attn_prepared(const sfa_attn_desc *d, const uint8_t *q_idx, const
     const AttnParams p = make_params(d, q_idx, q_val, k_idx, k_val, v, o, lse, ws);
     const int kern = resolve_kernel(d);
     if (kern == SFA_KERNEL_DECODE) return from_launch(launch_decode(p, d->d, d->d_v, st, ws));
-    if (kern == SFA_KERNEL_SM100_PAIR) return from_launch(launch_attn_sm100_pair(p, d->d, d->d_v, st, dbg));
-    if (kern == SFA_KERNEL_SM100_WIDE) return from_launch(launch_attn_sm100_wide(p, d->d, d->d_v, st, dbg));
     if (kern == SFA_KERNEL_SM100_OT) return from_launch(launch_attn_sm100_ot(p, d->d, d->d_v, st, dbg));
     if (kern == SFA_KERNEL_SM100_PP) return from_launch(launch_attn_sm100_pp(p, d->d, d->d_v, st, dbg));
     if (kern == SFA_KERNEL_SM100_OTH) return from_launch(launch_attn_sm100_oth(p, d->d, d->d_v, st, dbg));

@@ -68,10 +68,6 @@ cudaError_t launch_attn_simt(const AttnParams &p, bool bf16, int d, int d_v, cud
 // dbg (tests only, may be null): receives the raw 128x128 fp32 score tile S = Q~ K~^T of the
 // first key tile of work item 0, query tile 0.
 cudaError_t launch_attn_sm100(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
-// the same forward with M = 256 MMAs over CTA pairs (attn_sm100_pair.cu); d_v = 128 only
-cudaError_t launch_attn_sm100_pair(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
-// the same forward with 256-key score tiles and P apart from S (attn_sm100_wide.cu)
-cudaError_t launch_attn_sm100_wide(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
 cudaError_t launch_attn_sm100_ot(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
 // two query tiles in ping-pong, K~ by TMA from p.k_dense, P in TMEM (attn_sm100_pp.cu); R1, no window
 cudaError_t launch_attn_sm100_pp(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);

@@ -128,7 +128,11 @@ def test_n4_semantics_validation(sfa):
     for b in (dict(window=-1), dict(window=16, causal=False)):
         d = desc(sfa, **b)
         assert L.sfa_attn_fwd(ctypes.byref(d), *([ctypes.c_void_p(16)] * 8), 1 << 30, None) == 1, b
-    for kern in (sfa.KERNEL_SM100, sfa.KERNEL_SM100_PAIR, sfa.KERNEL_SM100_WIDE, sfa.KERNEL_DECODE):
+    # the round-1 ablation kernels PAIR / WIDE were removed in round 2: their numbers stay reserved
+    for kern in (sfa.KERNEL_SM100_PAIR, sfa.KERNEL_SM100_WIDE):
+        assert L.sfa_attn_fwd(ctypes.byref(desc(sfa, kernel=kern)), *([ctypes.c_void_p(16)] * 8), 1 << 30, None) == 3
+    for kern in (sfa.KERNEL_SM100, sfa.KERNEL_SM100_PAIR, sfa.KERNEL_SM100_WIDE, sfa.KERNEL_DECODE,
+                 sfa.KERNEL_SM100_PP, sfa.KERNEL_SM100_OTH):
         for b in (dict(edges_only=True), dict(window=16)):
             d = desc(sfa, kernel=kern, **b)
             assert L.sfa_attn_fwd(ctypes.byref(d), *([ctypes.c_void_p(16)] * 8), 1 << 30, None) == 3, (kern, b)

@@ -81,14 +81,13 @@ def test_peaked_rows_trigger_rescale(lib):
 
 
 # ---------------------------------------------------------------------------------------------
-# M = 256 CTA-pair kernel (attn_sm100_pair.cu): same checks
+# the other tensor-core kernels (attn_sm100_ot.cu default, _pp / _oth ablations): same checks
 # ---------------------------------------------------------------------------------------------
-VARIANTS = ["pair", "wide", "ot", "pp", "oth"]  # SFA_KERNEL_SM100_PAIR / _WIDE / _OT / _PP / _OTH
+VARIANTS = ["ot", "pp", "oth"]  # SFA_KERNEL_SM100_OT / _PP / _OTH
 
 
 def _kern(lib, name):
-    return {"pair": lib.KERNEL_SM100_PAIR, "wide": lib.KERNEL_SM100_WIDE, "ot": lib.KERNEL_SM100_OT,
-            "pp": lib.KERNEL_SM100_PP, "oth": lib.KERNEL_SM100_OTH}[name]
+    return {"ot": lib.KERNEL_SM100_OT, "pp": lib.KERNEL_SM100_PP, "oth": lib.KERNEL_SM100_OTH}[name]
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
@@ -115,14 +114,14 @@ def test_variant_score_tile_is_exact_overlap_sum(lib, variant, d, k):
     (2, 2, 2, 300, 64, 128, 8),     # MHA, d = 64, ragged
     (1, 2, 1, 515, 128, 128, 32),
     (1, 2, 2, 1, 128, 128, 4),      # a single token
-    (1, 2, 2, 700, 64, 64, 8),      # d_v = 64 (wide, pp)
+    (1, 2, 2, 700, 64, 64, 8),      # d_v = 64 (pp)
 ])
 @pytest.mark.parametrize("causal", [True, False])
 def test_variant_against_oracle(lib, variant, shape, causal):
     import torch
     B, H, H_kv, n, d, d_v, k = shape
-    if variant in ("pair", "ot", "oth") and d_v != 128:
-        pytest.skip("pair / ot kernels need d_v = 128 (M of the transposed product / split over the pair)")
+    if variant in ("ot", "oth") and d_v != 128:
+        pytest.skip("ot / oth kernels need d_v = 128 (M of the transposed product)")
     q, kx, v = host_qkv(56, B, H, H_kv, n, d, d_v, "bf16")
     qi, qv = oracle_codes(q, k)
     ki, kv = oracle_codes(kx, k)

@@ -47,6 +47,4 @@ if __name__ == "__main__":
     run(2, 8, 2, 3000, 128, 128, 16, "bf16", sfa.KERNEL_DECODE, n_q=1)         # decode shape
     run_bwd(1, 4, 2, 300, 128, 128, 16)                                        # backward kernels
     if "--no-ablations" not in sys.argv:  # CTA-pair / 256-key ablations last (synccheck stops at the pair kernel)
-        run(1, 4, 2, 520, 128, 128, 16, "bf16", sfa.KERNEL_SM100_PAIR)
-        run(1, 4, 2, 520, 128, 128, 16, "bf16", sfa.KERNEL_SM100_WIDE)
     print("sanitize smoke ok")

@@ -13,7 +13,7 @@ sys.path.insert(0, ROOT)
 from paper_2603_22300_b200 import inputs, sfa  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
-kern = {"sm100": sfa.KERNEL_SM100, "pair": sfa.KERNEL_SM100_PAIR, "wide": sfa.KERNEL_SM100_WIDE, "ot": sfa.KERNEL_SM100_OT,
+kern = {"sm100": sfa.KERNEL_SM100, "ot": sfa.KERNEL_SM100_OT,
         "pp": sfa.KERNEL_SM100_PP, "oth": sfa.KERNEL_SM100_OTH}[sys.argv[2] if len(sys.argv) > 2 else "sm100"]
 qwen = len(sys.argv) > 3 and sys.argv[3] == "qwen"  # bench config: causal, H=32, H_kv=8 (item 0 = last q block)
 B, H, H_kv, d, d_v, k = (1, 32, 8, 128, 128, 16) if qwen else (1, 2, 1, 128, 128, 16)
