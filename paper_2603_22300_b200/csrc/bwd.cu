@@ -214,6 +214,9 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
         // ---- epilogue (group 0): dQ~ row -> shared staging (the dead K~ ring) -> gather at the support
         mbar_wait(BAR(DQ_FULL), 0);
         tc_fence_after();
+        // the decompression warps' last K~ stores into the ring precede DQ_FULL through the MMA chain; the
+        // named barrier makes that ordering explicit (and visible to racecheck) before the ring is reused
+        named_bar_sync(6, 256);
         float *st = reinterpret_cast<float *>(gb + C::OFF_K) + (size_t)r * D;
 #pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
@@ -255,6 +258,7 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
             __syncwarp();
             if (lane == 0) mbar_arrive(BAR(K_FULL + s));
         }
+        asm volatile("bar.arrive 6, 256;" ::: "memory");  // done with the K~ ring (the epilogue reuses it)
     } else if (warp == 12) {
         // ==================== tcgen05.mma issuer ====================
         if (lane == 0) {
@@ -501,6 +505,9 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
             }
         }
         } else {
+        // the decompression warps' last Q~ stores precede the MMAs' completion; the named barrier makes the
+        // ordering explicit (and visible to racecheck) before the dead Q~ ring is reused as staging
+        named_bar_sync(6, 256);
 #pragma unroll 1
         for (int c = 0; c < D / 32; ++c) {
             uint32_t o[32];
@@ -556,6 +563,7 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
             __syncwarp();
             if (lane == 0) mbar_arrive(BAR(QQ_FULL + st));
         }
+        asm volatile("bar.arrive 6, 256;" ::: "memory");  // done with the Q~ ring (the dK~ epilogue reuses it)
     } else if (warp == 12) {
         // ==================== tcgen05.mma issuer ====================
         if (lane == 0 && ns > 0) {

@@ -46,5 +46,11 @@ if __name__ == "__main__":
     run(1, 2, 1, 200, 64, 64, 2, "f32", sfa.KERNEL_SIMT, edges_only=True)      # R2 on SIMT
     run(2, 8, 2, 3000, 128, 128, 16, "bf16", sfa.KERNEL_DECODE, n_q=1)         # decode shape
     run_bwd(1, 4, 2, 300, 128, 128, 16)                                        # backward kernels
-    if "--no-ablations" not in sys.argv:  # CTA-pair / 256-key ablations last (synccheck stops at the pair kernel)
+    # round 2: the persistent OT scheduler with more items than SMs (256 items: every CTA claims several),
+    # d = 64 keys, the fused Q + K top-k launch and the K~ rows, then the ablation kernels
+    run(4, 16, 4, 1024, 128, 128, 16, "bf16", sfa.KERNEL_AUTO)
+    run(2, 8, 2, 700, 64, 128, 8, "bf16", sfa.KERNEL_SM100_OT)
+    run(1, 4, 2, 300, 128, 128, 16, "bf16", sfa.KERNEL_SM100_PP)
+    run(1, 4, 2, 300, 128, 64, 16, "bf16", sfa.KERNEL_SM100_PP)
+    run(2, 8, 2, 700, 128, 128, 16, "bf16", sfa.KERNEL_SM100_OTH)
     print("sanitize smoke ok")
