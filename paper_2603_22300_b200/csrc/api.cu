@@ -351,9 +351,21 @@ sfa_status sfa_attn_fwd_fused_q(const sfa_attn_desc *desc, const void *q, const 
     return from_launch(launch_attn_sm100_ot(p, desc->d, desc->d_v, (cudaStream_t)stream, nullptr));
 }
 
+// backward workspace: D_i [B*H*n_q] fp32, then (256-aligned) the decompressed Q~ rows [B*H*n_q][d] and K~
+// rows [B*H_kv*n_kv][d], bf16, for the kernels' TMA
+struct BwdWs {
+    size_t qd, kd, total;
+};
+BwdWs bwd_ws(const sfa_attn_desc *d) {
+    BwdWs w;
+    w.qd = align_up((int64_t)d->B * d->H * d->n_q * sizeof(float), 256);
+    w.kd = w.qd + align_up((int64_t)d->B * d->H * d->n_q * d->d * 2, 256);
+    w.total = w.kd + align_up((int64_t)d->B * d->H_kv * d->n_kv * d->d * 2, 256);
+    return w;
+}
 size_t sfa_attn_bwd_workspace_bytes(const sfa_attn_desc *desc) {
     if (validate_desc(desc) != SFA_OK) return 0;
-    return (size_t)desc->B * desc->H * desc->n_q * sizeof(float);
+    return bwd_ws(desc).total;
 }
 
 sfa_status sfa_attn_bwd(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val, const uint8_t *k_idx,
@@ -372,8 +384,10 @@ sfa_status sfa_attn_bwd(const sfa_attn_desc *desc, const uint8_t *q_idx, const v
     if (workspace_bytes < sfa_attn_bwd_workspace_bytes(desc)) return SFA_ERR_RESOURCE;
     const AttnParams p = make_params(desc, q_idx, q_val, k_idx, k_val, v, const_cast<void *>(o),
                                      const_cast<float *>(lse), workspace);
-    return from_launch(launch_attn_bwd(p, desc->d, desc->d_v, dO, static_cast<float *>(workspace), dq_val, dk_val, dv,
-                                       (cudaStream_t)stream));
+    const BwdWs w = bwd_ws(desc);
+    uint8_t *ws = static_cast<uint8_t *>(workspace);
+    return from_launch(launch_attn_bwd(p, desc->d, desc->d_v, dO, static_cast<float *>(workspace), ws + w.qd, ws + w.kd,
+                                       dq_val, dk_val, dv, (cudaStream_t)stream));
 }
 
 sfa_status sfa_debug_sm100_scores(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val,

@@ -21,6 +21,7 @@
 // rounded to bf16 for the tensor cores (reading A24: the gradient tolerance is componentwise).
 // Operands: codes decompressed on chip into 128B-swizzled tiles (densify.cuh), V and dO by TMA.
 #include <cudaTypedefs.h>
+#include <cstring>
 #include <mutex>
 #include <type_traits>
 
@@ -40,6 +41,12 @@ constexpr int BM = 128, BN = 128, NTH = 448;
 // two such warps (the exponentials and the TMEM traffic of one hide the latency of the other);
 // warps 8-11 decompression; warp 12 tcgen05.mma issuer + TMEM owner; warp 13 TMA.
 constexpr int ROW_WARPS = 8;
+// 1: Q~ and K~ tiles arrive by TMA from rows decompressed once per row (k_dense_kernel, vprep.cu) --
+// the on-chip decompression (zero fill + k u16 stores per row per tile) was ~40 % of the dK/dV kernel's
+// shared-memory LSU traffic and most of its 440 M bank conflicts; 0: decompression warps, as round 1
+#ifndef SFA_BWD_TMA
+#define SFA_BWD_TMA 1
+#endif
 
 // TMEM column of the packed bf16 operand (P, P^T, dS or dS^T) for the K-step kk (16 rows of K):
 // group g writes its 64 columns' worth of bf16 pairs into [64g, 64g + 32) over scores it has read
@@ -104,7 +111,9 @@ __device__ __forceinline__ uint32_t dq_sbuf(int j) { return (j & 1) ? 384u : 0u;
 
 template <int D, int DV>
 __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ CUtensorMap tm_v,
-                                                        const __grid_constant__ CUtensorMap tm_do, const BwdArgs a) {
+                                                        const __grid_constant__ CUtensorMap tm_do,
+                                                        const __grid_constant__ CUtensorMap tm_q,
+                                                        const __grid_constant__ CUtensorMap tm_k, const BwdArgs a) {
     using C = DqCfg<D, DV>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_s = smem_u32(smem_raw);
@@ -131,7 +140,7 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NBAR_DQ; ++i)
-            mbar_init(BAR(i), (i == Q_FULL || i == K_FULL || i == K_FULL + 1 || i == K_FULL + 2) ? 4u
+            mbar_init(BAR(i), (i == Q_FULL || i == K_FULL || i == K_FULL + 1 || i == K_FULL + 2) ? (SFA_BWD_TMA ? 1u : 4u)
                               : ((i == DS_READY || i == DP_FREE) ? 8u : 1u));
         fence_mbar_init();
     }
@@ -139,6 +148,10 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
     if (warp == 13 && lane == 0) {
         tma_prefetch_desc(&tm_v);
         tma_prefetch_desc(&tm_do);
+        if (SFA_BWD_TMA) {
+            tma_prefetch_desc(&tm_q);
+            tma_prefetch_desc(&tm_k);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -233,9 +246,27 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
             }
         }
     } else if (warp < 12) {
-        // ==================== decompression: Q~ once, K~ per key tile (thread = row) ====================
+        // ==================== Q~ once, K~ per key tile: TMA (warp 8, lane 0) or decompression ====================
         const int r = threadIdx.x - 32 * ROW_WARPS;
         const int k = a.k;
+        if (SFA_BWD_TMA) {
+            if (warp == ROW_WARPS && lane == 0) {
+                mbar_arrive_expect_tx(BAR(Q_FULL), BM * D * 2);
+#pragma unroll
+                for (int cb = 0; cb < D / 64; ++cb)
+                    tma_load_3d(sb + C::OFF_Q + cb * BM * 128, &tm_q, BAR(Q_FULL), cb * 64, ib * BM, b * a.H + h);
+                for (int j = 0; j < nt; ++j) {
+                    const int s = j % C::NK, u = j / C::NK;
+                    mbar_wait(BAR(K_EMPTY + s), (u & 1) ^ 1);
+                    mbar_arrive_expect_tx(BAR(K_FULL + s), BN * D * 2);
+#pragma unroll
+                    for (int cb = 0; cb < D / 64; ++cb)
+                        tma_load_3d(sb + C::OFF_K + s * BN * D * 2 + cb * BN * 128, &tm_k, BAR(K_FULL + s), cb * 64,
+                                    j * BN, b * a.H_kv + g);
+                }
+            }
+            __syncwarp();
+        } else {
         {
             const int64_t i = (int64_t)ib * BM + r;
             const bool ok = i < a.n_q;
@@ -257,6 +288,7 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dq_kernel(const __grid_constant__ 
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(BAR(K_FULL + s));
+        }
         }
         asm volatile("bar.arrive 6, 256;" ::: "memory");  // done with the K~ ring (the epilogue reuses it)
     } else if (warp == 12) {
@@ -357,7 +389,9 @@ enum { KK_FULL = 0, KV_FULL, QQ_FULL, QQ_EMPTY = QQ_FULL + 3, DOO_FULL = QQ_EMPT
 
 template <int D, int DV>
 __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tm_v,
-                                                          const __grid_constant__ CUtensorMap tm_do, const BwdArgs a) {
+                                                          const __grid_constant__ CUtensorMap tm_do,
+                                                          const __grid_constant__ CUtensorMap tm_q,
+                                                          const __grid_constant__ CUtensorMap tm_k, const BwdArgs a) {
     using C = KvCfg<D, DV>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_s = smem_u32(smem_raw);
@@ -383,7 +417,8 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < NBAR_KV; ++i)
-            mbar_init(BAR(i), (i == KK_FULL || i == QQ_FULL || i == QQ_FULL + 1 || i == QQ_FULL + 2) ? 4u
+            mbar_init(BAR(i), i == KK_FULL ? (SFA_BWD_TMA ? 1u : 4u)
+                              : (i == QQ_FULL || i == QQ_FULL + 1 || i == QQ_FULL + 2) ? 4u
                               : ((i == P_READY || i == KDS_READY) ? 8u : 1u));
         fence_mbar_init();
     }
@@ -391,6 +426,10 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
     if (warp == 13 && lane == 0) {
         tma_prefetch_desc(&tm_v);
         tma_prefetch_desc(&tm_do);
+        if (SFA_BWD_TMA) {
+            tma_prefetch_desc(&tm_q);
+            tma_prefetch_desc(&tm_k);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -528,26 +567,35 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
             }
         }
     } else if (warp < 12) {
-        // ==================== decompression: K~ once, Q~ (+ LSE, D) per step (thread = row) ====================
+        // ============ K~ once, Q~ (+ LSE, D staging) per step: TMA (warp 8, lane 0) or decompression ============
         const int r = threadIdx.x - 32 * ROW_WARPS;
         const int k = a.k;
         const int64_t kv0 = ((int64_t)b * a.H_kv + g) * a.n_kv;
-        {
-            const int64_t key = (int64_t)jb * BN + r;
-            const bool ok = key < a.n_kv;
-            const int64_t kr = kv0 + (ok ? key : 0);
-            densify_row<D>(sb + C::OFF_K, BN, r, ok, a.k_idx + kr * k, a.k_val + kr * k, k);
+        if (SFA_BWD_TMA) {
+            if (warp == ROW_WARPS && lane == 0) {
+                mbar_arrive_expect_tx(BAR(KK_FULL), BN * D * 2);
+#pragma unroll
+                for (int cb = 0; cb < D / 64; ++cb)
+                    tma_load_3d(sb + C::OFF_K + cb * BN * 128, &tm_k, BAR(KK_FULL), cb * 64, jb * BN, b * a.H_kv + g);
+            }
+        } else {
+            {
+                const int64_t key = (int64_t)jb * BN + r;
+                const bool ok = key < a.n_kv;
+                const int64_t kr = kv0 + (ok ? key : 0);
+                densify_row<D>(sb + C::OFF_K, BN, r, ok, a.k_idx + kr * k, a.k_val + kr * k, k);
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(BAR(KK_FULL));
         }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(BAR(KK_FULL));
         for (int s = 0; s < ns; ++s) {
             const int st = s % C::NQ, u = s / C::NQ;
             const int h = g * R + s / nib, ib = ib0 + s % nib;
             const int64_t i = (int64_t)ib * BM + r;
             const bool ok = i < a.n_q;
             const int64_t row = ((int64_t)b * a.H + h) * a.n_q + (ok ? i : 0);
-            if (s + 1 < ns) {  // next step's query codes (and LSE, D) into L1
+            if (!SFA_BWD_TMA && s + 1 < ns) {  // next step's query codes (and LSE, D) into L1
                 const int h1 = g * R + (s + 1) / nib, ib1 = ib0 + (s + 1) % nib;
                 const int64_t i1 = (int64_t)ib1 * BM + r;
                 if (i1 < a.n_q) {
@@ -556,7 +604,17 @@ __global__ void __launch_bounds__(NTH, 1) bwd_dkdv_kernel(const __grid_constant_
                 }
             }
             mbar_wait(BAR(QQ_EMPTY + st), (u & 1) ^ 1);
-            densify_row<D>(sb + C::OFF_Q + st * BM * D * 2, BM, r, ok, a.q_idx + row * k, a.q_val + row * k, k);
+            if (SFA_BWD_TMA) {  // the Q~ tile by TMA; its bytes join this stage's four warp arrivals
+                if (warp == ROW_WARPS && lane == 0) {
+                    mbar_expect_tx(BAR(QQ_FULL + st), BM * D * 2);
+#pragma unroll
+                    for (int cb = 0; cb < D / 64; ++cb)
+                        tma_load_3d(sb + C::OFF_Q + st * BM * D * 2 + cb * BM * 128, &tm_q, BAR(QQ_FULL + st), cb * 64,
+                                    ib * BM, b * a.H + h);
+                }
+            } else {
+                densify_row<D>(sb + C::OFF_Q + st * BM * D * 2, BM, r, ok, a.q_idx + row * k, a.q_val + row * k, k);
+            }
             ldv[st * 2 * BM + r] = ok ? __ldg(a.lse + row) * 1.4426950408889634f : 0.f;
             ldv[st * 2 * BM + BM + r] = ok ? __ldg(a.Dr + row) : 0.f;
             fence_proxy_async_smem();
@@ -672,7 +730,8 @@ bool make_map(CUtensorMap *tm, const void *base, int dv, int64_t rows, int64_t p
 }
 
 template <int D, int DV>
-cudaError_t launch_bwd_t(const BwdArgs &a, const CUtensorMap &tv, const CUtensorMap &tdo, cudaStream_t st) {
+cudaError_t launch_bwd_t(const BwdArgs &a, const CUtensorMap &tv, const CUtensorMap &tdo, const CUtensorMap &tq,
+                         const CUtensorMap &tk, cudaStream_t st) {
     using CQ = DqCfg<D, DV>;
     using CK = KvCfg<D, DV>;
     auto kq = bwd_dq_kernel<D, DV>;
@@ -683,18 +742,23 @@ cudaError_t launch_bwd_t(const BwdArgs &a, const CUtensorMap &tv, const CUtensor
     if (e != cudaSuccess) return e;
     const int64_t nq_items = (int64_t)a.B * a.H * a.nqb, nk_items = (int64_t)a.B * a.H_kv * a.nkt;
     if (nq_items > INT32_MAX || nk_items > INT32_MAX) return cudaErrorNotSupported;
-    if (nk_items > 0) kk<<<(unsigned)nk_items, NTH, CK::SMEM, st>>>(tv, tdo, a);
+    if (nk_items > 0) kk<<<(unsigned)nk_items, NTH, CK::SMEM, st>>>(tv, tdo, tq, tk, a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    if (nq_items > 0) kq<<<(unsigned)nq_items, NTH, CQ::SMEM, st>>>(tv, tdo, a);
+    if (nq_items > 0) kq<<<(unsigned)nq_items, NTH, CQ::SMEM, st>>>(tv, tdo, tq, tk, a);
     return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_attn_bwd(const AttnParams &p, int d, int d_v, const void *dO, float *Dws, float *dq, float *dk,
-                            float *dv, cudaStream_t st) {
+cudaError_t launch_attn_bwd(const AttnParams &p, int d, int d_v, const void *dO, float *Dws, void *qd, void *kd,
+                            float *dq, float *dk, float *dv, cudaStream_t st) {
     if ((d != 64 && d != 128) || (d_v != 64 && d_v != 128)) return cudaErrorNotSupported;
+    if (SFA_BWD_TMA) {  // Q~ and K~ rows, decompressed once per row for the kernels' TMA
+        cudaError_t e = launch_kdense(p.q_idx, p.q_val, (int64_t)p.B * p.H * p.n_q, d, p.k, qd, st);
+        if (e == cudaSuccess) e = launch_kdense(p.k_idx, p.k_val, (int64_t)p.B * p.H_kv * p.n_kv, d, p.k, kd, st);
+        if (e != cudaSuccess) return e;
+    }
     const int64_t rows = (int64_t)p.B * p.H * p.n_q;
     if (rows > 0) {
         bwd_prep_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(static_cast<const uint16_t *>(p.o),
@@ -724,11 +788,16 @@ cudaError_t launch_attn_bwd(const AttnParams &p, int d, int d_v, const void *dO,
     a.nkt = (int)((p.n_kv + BN - 1) / BN);
     a.c_scale = p.scale_log2;
     a.scale = p.scale_log2 / 1.4426950408889634f;
-    CUtensorMap tv, tdo;
+    CUtensorMap tv, tdo, tq, tk;
+    memset(&tq, 0, sizeof(tq));
+    memset(&tk, 0, sizeof(tk));
     if (!make_map(&tv, p.v, d_v, p.n_kv, (int64_t)p.B * p.H_kv) || !make_map(&tdo, dO, d_v, p.n_q, (int64_t)p.B * p.H))
         return cudaErrorInvalidValue;
-    if (d == 64) return d_v == 64 ? launch_bwd_t<64, 64>(a, tv, tdo, st) : launch_bwd_t<64, 128>(a, tv, tdo, st);
-    return d_v == 64 ? launch_bwd_t<128, 64>(a, tv, tdo, st) : launch_bwd_t<128, 128>(a, tv, tdo, st);
+    if (SFA_BWD_TMA &&
+        (!make_map(&tq, qd, d, p.n_q, (int64_t)p.B * p.H) || !make_map(&tk, kd, d, p.n_kv, (int64_t)p.B * p.H_kv)))
+        return cudaErrorInvalidValue;
+    if (d == 64) return d_v == 64 ? launch_bwd_t<64, 64>(a, tv, tdo, tq, tk, st) : launch_bwd_t<64, 128>(a, tv, tdo, tq, tk, st);
+    return d_v == 64 ? launch_bwd_t<128, 64>(a, tv, tdo, tq, tk, st) : launch_bwd_t<128, 128>(a, tv, tdo, tq, tk, st);
 }
 
 }  // namespace sfa

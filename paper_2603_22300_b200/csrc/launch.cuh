@@ -75,7 +75,8 @@ cudaError_t launch_attn_sm100_pp(const AttnParams &p, int d, int d_v, cudaStream
 cudaError_t launch_attn_sm100_oth(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg);
 // backward with the straight-through rule (bwd.cu): D = rowsum(dO . O) into Dws [B*H*n_q], then the
 // dK~/dV and dQ~ tensor-core kernels; gradients w.r.t. the code values and V, fp32
-cudaError_t launch_attn_bwd(const AttnParams &p, int d, int d_v, const void *dO, float *Dws, float *dq, float *dk,
-                            float *dv, cudaStream_t st);
+// qd / kd: workspace for the decompressed Q~ / K~ rows (bf16 [rows][d]) the kernels' TMA reads
+cudaError_t launch_attn_bwd(const AttnParams &p, int d, int d_v, const void *dO, float *Dws, void *qd, void *kd,
+                            float *dq, float *dk, float *dv, cudaStream_t st);
 
 }  // namespace sfa

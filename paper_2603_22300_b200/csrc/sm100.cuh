@@ -26,6 +26,11 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t byt
                  "r"(bytes)
                  : "memory");
 }
+// raise the pending transaction count of the current phase without arriving (a TMA load whose bytes this
+// phase must also wait for, issued by one of the barrier's regular arrivers before its own arrive)
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
 // Wait until the phase with the given parity has completed.  On a freshly initialised barrier,
 // parity 1 returns immediately (the "previous" phase counts as complete): producers start there.
 #ifndef SFA_WATCHDOG
