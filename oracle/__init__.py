@@ -43,7 +43,7 @@ def _load():
         _lib.ref_topk_codes.argtypes = [P, I, L, I, I, P, P]
         _lib.ref_topk_codes.restype = I
         _lib.ref_attn_fwd.argtypes = [I, I, I, I, I, I, L, L, L, I, D, I, P, P, P, P, P, P, L, P, P, I]
-        _lib.ref_attn_fwd_ex.argtypes = [I, I, I, I, I, I, L, L, L, I, D, I, P, P, P, P, P, P, L, P, P, I, I, L]
+        _lib.ref_attn_fwd_ex.argtypes = [I, I, I, I, I, I, L, L, L, I, D, I, P, P, P, P, P, P, L, P, P, I, I, L, P, I]
         _lib.ref_attn_fwd.restype = I
         _lib.ref_scores_row.argtypes = [I, I, I, I, I, L, L, L, I, D, I, P, P, P, P, L, P]
         _lib.ref_scores_row.restype = I
@@ -87,14 +87,17 @@ def topk_codes(x: np.ndarray, k: int):
 
 
 def attn_fwd(q_idx, q_val, k_idx, k_val, v, *, d, causal=True, scale=None, q_pos0=0, rows=None,
-             threads=None, edges_only=False, window=0):
+             threads=None, edges_only=False, window=0, block_sel=None):
     """Plain fp64 SFA attention forward on the decompressed codes (sfa_oracle.c ref_attn_fwd).
 
     q_idx/q_val [B,H,n_q,k]; k_idx/k_val [B,H_kv,n_kv,k]; v [B,H_kv,n_kv,d_v] (vals and v share a
     dtype: float32 or uint16 bf16 bits).  ``d`` is the full head dimension.  ``rows``: optional
     int64 flat row ids into [B,H,n_q].  ``edges_only``: reading A1/R2 --
     only pairs whose supports intersect enter the softmax.  ``window`` > 0: causal sliding window (SURVEY
-    8(f) N4), key j also needs j > q_pos0 + i - window.  Returns fp64 (o, lse), shaped [B,H,n_q,(d_v)] or [nsel,(d_v)].
+    8(f) N4), key j also needs j > q_pos0 + i - window.  ``block_sel`` int32 [B,H_kv,ceil(n_q/128),max_sel]
+    (NSA-style block selection, SURVEY 8(f) N4): key j also needs its block j // 128 in the list of the
+    row's query block i // 128 (entries < 0 are padding).  Returns fp64 (o, lse), shaped [B,H,n_q,(d_v)]
+    or [nsel,(d_v)].
     """
     q_idx = np.ascontiguousarray(q_idx); q_val = np.ascontiguousarray(q_val)
     k_idx = np.ascontiguousarray(k_idx); k_val = np.ascontiguousarray(k_val)
@@ -116,9 +119,15 @@ def attn_fwd(q_idx, q_val, k_idx, k_val, v, *, d, causal=True, scale=None, q_pos
         o = np.zeros((nsel, d_v), np.float64)
         lse = np.zeros((nsel,), np.float64)
     threads = threads or os.cpu_count() or 1
+    bs, max_sel = None, 0
+    if block_sel is not None:
+        bs = np.ascontiguousarray(block_sel, dtype=np.int32)
+        assert bs.shape[:3] == (B, H_kv, (n_q + 127) // 128), bs.shape
+        max_sel = bs.shape[3]
     st = _load().ref_attn_fwd_ex(B, H, H_kv, d, k, d_v, n_q, n_kv, q_pos0, int(bool(causal)), float(scale), dt,
                                  _ptr(q_idx), _ptr(q_val), _ptr(k_idx), _ptr(k_val), _ptr(v), _ptr(sel), nsel,
-                                 _ptr(o), _ptr(lse), int(threads), int(bool(edges_only)), int(window))
+                                 _ptr(o), _ptr(lse), int(threads), int(bool(edges_only)), int(window), _ptr(bs),
+                                 int(max_sel))
     if st:
         raise OracleError(st)
     return o, lse

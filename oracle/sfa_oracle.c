@@ -44,6 +44,12 @@
  *                      j > q_pos0 + i - w          (the last w positions up to and including i)
  *                    Rows with no allowed key: O = 0, LSE = -inf (A10).
  *
+ *                    block_sel (composition with block-level token selection: NSA-style
+ *                    "select the key blocks each query block attends"): with blocks of
+ *                    128 positions, key j is allowed only if, in addition, its block j / 128 appears in
+ *                    the list block_sel[b][g][i / 128][0 .. max_sel) of the row's (batch, kv head, local
+ *                    query block); entries < 0 are padding.  Rows with no allowed key: O = 0, LSE = -inf.
+ *
  *   ref_scores_row   the s_ij of one row (for the "rows of P sum to 1" pin).
  *
  *   ref_attn_bwd     the backward pass of ref_attn_fwd with the straight-through rule
@@ -155,6 +161,8 @@ int ref_topk_codes(const void *x, int dtype, int64_t rows, int d, int k, uint8_t
 typedef struct {
     int B, H, H_kv, d, k, d_v, causal, dtype, edges_only;
     int64_t n_q, n_kv, q_pos0, window;
+    const int32_t *bsel; /* nullable: [B][H_kv][ceil(n_q/128)][max_sel] key-block lists */
+    int max_sel;
     double scale;
     const uint8_t *q_idx, *k_idx;
     const void *q_val, *k_val, *v;
@@ -179,6 +187,15 @@ static int supports_intersect(const uint8_t *q_idx, int64_t qrow, const uint8_t 
     return 0;
 }
 
+/* block selection: is key j's block in the list of (b, g, query block of local row i)? */
+static int block_selected(const attn_job *J, int b, int g, int64_t i, int64_t j) {
+    int64_t nqb = (J->n_q + 127) / 128;
+    const int32_t *L = J->bsel + (((int64_t)b * J->H_kv + g) * nqb + i / 128) * J->max_sel;
+    for (int t = 0; t < J->max_sel; ++t)
+        if (L[t] >= 0 && (int64_t)L[t] == j / 128) return 1;
+    return 0;
+}
+
 static void attn_one_row(attn_job *J, int64_t flat, double *o, double *lse, double *qd, double *kd, double *s) {
     int64_t i = flat % J->n_q;
     int64_t bh = flat / J->n_q;
@@ -197,8 +214,9 @@ static void attn_one_row(attn_job *J, int64_t flat, double *o, double *lse, doub
     densify(J->q_idx, J->q_val, J->dtype, flat, J->k, J->d, qd);
     double m = -INFINITY;
     for (int64_t j = 0; j <= jmax; ++j) {
-        if (j < jmin || (J->edges_only && !supports_intersect(J->q_idx, flat, J->k_idx, kvrow0 + j, J->k))) {
-            s[j] = -INFINITY; /* R2: not an edge -> excluded from the softmax */
+        if (j < jmin || (J->edges_only && !supports_intersect(J->q_idx, flat, J->k_idx, kvrow0 + j, J->k)) ||
+            (J->bsel && !block_selected(J, b, g, i, j))) {
+            s[j] = -INFINITY; /* R2: not an edge / block not selected -> excluded from the softmax */
             continue;
         }
         densify(J->k_idx, J->k_val, J->dtype, kvrow0 + j, J->k, J->d, kd);
@@ -207,7 +225,7 @@ static void attn_one_row(attn_job *J, int64_t flat, double *o, double *lse, doub
         s[j] = J->scale * acc; /* A5/A17: scale applied after the sum */
         if (s[j] > m) m = s[j];
     }
-    if (m == -INFINITY) { /* R2 only: no edge in the row (as A10) */
+    if (m == -INFINITY) { /* R2 / block selection: no allowed key in the row (as A10) */
         *lse = -INFINITY;
         return;
     }
@@ -253,8 +271,9 @@ static void *attn_worker(void *arg) {
 int ref_attn_fwd_ex(int B, int H, int H_kv, int d, int k, int d_v, int64_t n_q, int64_t n_kv, int64_t q_pos0,
                     int causal, double scale, int dtype, const uint8_t *q_idx, const void *q_val,
                     const uint8_t *k_idx, const void *k_val, const void *v, const int64_t *sel, int64_t nsel,
-                    double *o, double *lse, int threads, int edges_only, int64_t window) {
-    if (window < 0) return ORACLE_INVALID_ARGUMENT;
+                    double *o, double *lse, int threads, int edges_only, int64_t window, const int32_t *bsel,
+                    int max_sel) {
+    if (window < 0 || (bsel && max_sel < 1)) return ORACLE_INVALID_ARGUMENT;
     if (B < 1 || H < 1 || H_kv < 1 || H % H_kv || d < 1 || d > 256 || k < 1 || k > d || d_v < 1 || n_q < 0 ||
         n_kv < 0 || dtype < 0 || dtype > 2 || !(scale > 0) || !isfinite(scale))
         return ORACLE_INVALID_ARGUMENT;
@@ -264,6 +283,8 @@ int ref_attn_fwd_ex(int B, int H, int H_kv, int d, int k, int d_v, int64_t n_q, 
     J.n_q = n_q; J.n_kv = n_kv; J.q_pos0 = q_pos0; J.scale = scale;
     J.edges_only = edges_only != 0;
     J.window = window;
+    J.bsel = bsel;
+    J.max_sel = max_sel;
     J.q_idx = q_idx; J.k_idx = k_idx; J.q_val = q_val; J.k_val = k_val; J.v = v;
     J.sel = sel;
     J.nsel = sel ? nsel : (int64_t)B * H * n_q;
@@ -283,7 +304,7 @@ int ref_attn_fwd(int B, int H, int H_kv, int d, int k, int d_v, int64_t n_q, int
                  const uint8_t *k_idx, const void *k_val, const void *v, const int64_t *sel, int64_t nsel,
                  double *o, double *lse, int threads) {
     return ref_attn_fwd_ex(B, H, H_kv, d, k, d_v, n_q, n_kv, q_pos0, causal, scale, dtype, q_idx, q_val, k_idx,
-                           k_val, v, sel, nsel, o, lse, threads, 0, 0);
+                           k_val, v, sel, nsel, o, lse, threads, 0, 0, NULL, 0);
 }
 
 /* s_ij for j = 0..n_kv-1 of one query row (flat id into [B][H][n_q]); masked keys get -inf. */
