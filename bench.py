@@ -59,7 +59,9 @@ def parse():
     ap.add_argument("--fused-q", action="store_true",
                     help="step 1 on Q inside the attention prologue (sfa_attn_fwd_fused_q, N3(ii) ablation)")
     ap.add_argument("--k", type=int, default=None, help="override the code size k (sweep)")
-    ap.add_argument("--mode", default="forward", choices=["forward", "decode", "bwd"],
+    ap.add_argument("--blocks", type=int, default=8,
+                    help="--mode blocksel: key blocks (of 128) each query block selects (its diagonal + earlier ones)")
+    ap.add_argument("--mode", default="forward", choices=["forward", "decode", "bwd", "blocksel"],
                     help="decode: SURVEY 8(f) N2, one new query row per sequence over a cached K/V of the config's n")
     ap.add_argument("--decode-batch", type=int, default=8, help="sequences per GPU in --mode decode")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
@@ -316,6 +318,104 @@ def run_bwd(args, W, rank, world, local):
                              "traffic": None, "flops_per_pair": 8 * d + 6 * d_v,
                              "mufu_floor_ms": 2 * pairs / (N_SMS * MUFU_EX2_PER_CLK_SM * pk["sm_max_mhz"] * 1e6) * 1e3},
                 "cpu_baseline": None, "e2e": None, "gpu_launches": 3 * args.steps, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+
+
+def run_blocksel(args, W, rank, world, local):
+    """the forward composed with NSA-style block selection (sfa_attn_fwd_blocksel): every
+    query block of 128 rows attends its diagonal key block and --blocks - 1 earlier ones (spread evenly,
+    deterministic), intersected with the causal mask.  The step is stage 1 (Q + K codes, one launch) +
+    step 3 + the attention over the listed tiles.  Context: the full causal SFA step on the same inputs."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_2603_22300_b200 import inputs, sfa
+    dev = torch.device("cuda", local)
+    B, H, H_kv, n, d, d_v, k = W.B, W.H, W.H_kv, W.n, W.d, W.d_v, W.k
+    seed = accounting.SEEDS[args.config]
+    bf = torch.bfloat16
+    Q = sfa.gen_fill(torch.empty((B, H, n, d), dtype=bf, device=dev), seed, inputs.TID_Q)
+    K = sfa.gen_fill(torch.empty((B, H_kv, n, d), dtype=bf, device=dev), seed, inputs.TID_K)
+    V = sfa.gen_fill(torch.empty((B, H_kv, n, d_v), dtype=bf, device=dev), seed, inputs.TID_V)
+    nqb = (n + 127) // 128
+    S = max(1, args.blocks)
+    sel = np.full((B, H_kv, nqb, S), -1, np.int32)
+    for qb in range(nqb):  # the diagonal block + S - 1 earlier ones spread evenly over [0, qb)
+        chosen = sorted(set([int(x) for x in np.linspace(0, qb - 1, S - 1)] if qb > 0 and S > 1 else []) | {qb})
+        sel[:, :, qb, :len(chosen)] = chosen
+    sel_t = torch.from_numpy(sel).to(dev)
+    selected_pairs = 0  # allowed pairs: causal within the listed blocks
+    for qb in range(nqb):
+        rows = min(128, n - qb * 128)
+        for t in sel[0, 0, qb]:
+            if t < 0:
+                continue
+            if t < qb:
+                selected_pairs += rows * min(128, n - t * 128)
+            elif t == qb:
+                selected_pairs += rows * (rows + 1) // 2
+    selected_pairs *= B * H
+    qi = torch.empty((B, H, n, k), dtype=torch.uint8, device=dev); qv = torch.empty((B, H, n, k), dtype=bf, device=dev)
+    ki = torch.empty((B, H_kv, n, k), dtype=torch.uint8, device=dev); kv = torch.empty((B, H_kv, n, k), dtype=bf, device=dev)
+    desc = sfa.make_desc(B=B, H=H, H_kv=H_kv, d=d, k=k, d_v=d_v, n_q=n, n_kv=n, causal=True)
+    L = sfa.lib()
+    ws = torch.empty(sfa.workspace_bytes(desc), dtype=torch.uint8, device=dev)
+    O = torch.empty((B, H, n, d_v), dtype=bf, device=dev); LSE = torch.empty((B, H, n), dtype=torch.float32, device=dev)
+    flush = torch.empty(L2_FLUSH_MB * 2 ** 20, dtype=torch.uint8, device=dev)
+    P_ = lambda t: ctypes.c_void_p(t.data_ptr())
+    st = lambda: ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def step(full, ev=None):
+        if ev: ev[0].record()
+        r1 = L.sfa_topk_codes_qk(P_(Q), B * H * n, d, P_(qi), P_(qv), P_(K), B * H_kv * n, d, P_(ki), P_(kv),
+                                 desc.dtype, d, k, None, st())
+        if ev: ev[1].record()
+        if full:
+            r2 = L.sfa_attn_fwd(ctypes.byref(desc), P_(qi), P_(qv), P_(ki), P_(kv), P_(V), P_(O), P_(LSE), P_(ws),
+                                ws.numel(), st())
+        else:
+            r2 = L.sfa_attn_fwd_blocksel(ctypes.byref(desc), P_(qi), P_(qv), P_(ki), P_(kv), P_(V), P_(sel_t), S,
+                                         P_(O), P_(LSE), P_(ws), ws.numel(), st())
+        if ev: ev[2].record()
+        if r1 or r2:
+            raise RuntimeError(f"sfa call failed: {(r1, r2)}")
+
+    def timed(full):
+        for _ in range(args.warmup):
+            flush.zero_()
+            step(full)
+        torch.cuda.synchronize()
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+        with ClockSampler(local) as clk:
+            for e in evs:
+                flush.zero_()
+                step(full, e)
+            torch.cuda.synchronize()
+        tot = sum(e[0].elapsed_time(e[2]) for e in evs) / args.steps
+        att = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+        return tot, att, clk.summary()
+
+    ms, att_ms, clocks = timed(False)
+    full_ms, full_att_ms, _ = timed(True)
+    pk = peaks()
+    mufu_peak = N_SMS * MUFU_EX2_PER_CLK_SM * pk["sm_max_mhz"] * 1e6
+    if rank == 0:
+        line = {"metric": "FlashSFA fwd with NSA-style block selection, ms & tokens/s (SURVEY 8(f) N4)",
+                "value": B * n / (ms / 1e3), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded generator on device)",
+                "config": {"workload": f"{args.config}: B={B}, H={H}, H_kv={H_kv}, n={n}, d={d}, d_v={d_v}, k={k}, "
+                                       f"causal, {S} key blocks of 128 per query block (diagonal + {S - 1} earlier)",
+                           "global_batch": B, "seq_len": n, "l2": f"explicit {L2_FLUSH_MB} MB write between steps"},
+                "stage_ms": {"topk_qk": ms - att_ms, "prepare_and_attn": att_ms},
+                "selected_pairs": selected_pairs,
+                "roofline": {"bound": "alu", "kernel": "attn_sm100_ot_kernel<BSEL>", "unit": "G pairs/s",
+                             "achieved": selected_pairs / (att_ms / 1e3) / 1e9, "peak": mufu_peak / 1e9,
+                             "frac": selected_pairs / (att_ms / 1e3) / mufu_peak},
+                "context": {"full_causal_step_ms": full_ms, "full_causal_prepare_and_attn_ms": full_att_ms},
+                "cpu_baseline": None, "e2e": None, "gpu_launches": 6 * args.steps, "clocks": clocks}
         print(json.dumps(line), flush=True)
 
 
@@ -602,6 +702,9 @@ def main():
         run_bwd(args, W, rank, world, local)
         if world > 1:
             dist.destroy_process_group()
+        return
+    if args.mode == "blocksel":
+        run_blocksel(args, W, rank, world, local)
         return
     if args.mode == "decode":
         if world > 1:

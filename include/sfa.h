@@ -163,6 +163,21 @@ SFA_API sfa_status sfa_attn_fwd_prepared(const sfa_attn_desc *desc, const uint8_
                                          const uint8_t *k_idx, const void *k_val, const void *v, void *o, float *lse,
                                          const void *workspace, size_t workspace_bytes, sfa_stream_t stream);
 
+/* FlashSFA forward composed with block-level token selection (NSA-style "each query
+ * block attends the key blocks it selected", "SFA is orthogonal to token-level sparsity").
+ *   block_sel [B][H_kv][ceil(n_q/128)][max_sel] int32, device: for each (batch, kv head, block of 128
+ *             query rows) the indices of the 128-key blocks it may attend, ASCENDING, padded with -1
+ *             (entries past the first negative one are ignored); intersected with the causal mask.
+ *   Key j is allowed for query row i iff j <= q_pos0 + i (if causal) and j / 128 is listed for the
+ *   row's query block i / 128; rows without an allowed key get O = 0, LSE = -inf.  Runs steps 3-8 on
+ *   the default tensor-core kernel (persistent tile scheduler over the listed tiles only).
+ *   Supported: bf16, d_v = 128, H / H_kv even, edges_only = 0, window = 0, kernel AUTO or SM100_OT;
+ *   else SFA_ERR_UNSUPPORTED.  max_sel >= 1; block_sel 4-byte aligned.  Workspace as sfa_attn_fwd. */
+SFA_API sfa_status sfa_attn_fwd_blocksel(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val,
+                                         const uint8_t *k_idx, const void *k_val, const void *v,
+                                         const int32_t *block_sel, int32_t max_sel, void *o, float *lse,
+                                         void *workspace, size_t workspace_bytes, sfa_stream_t stream);
+
 /* Steps 1 (on Q) to 8 in one kernel: the attention prologue selects the top-k of
  * every DENSE query row itself (the same selection code as sfa_topk_codes, so the support and the result
  * are bit-identical to sfa_topk_codes + sfa_attn_fwd_prepared), builds Q~ on chip and, if q_idx_out /

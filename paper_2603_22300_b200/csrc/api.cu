@@ -330,6 +330,30 @@ sfa_status sfa_attn_fwd_prepared(const sfa_attn_desc *desc, const uint8_t *q_idx
     return run_attn_prepared(desc, q_idx, q_val, k_idx, k_val, v, o, lse, (void *)workspace, (cudaStream_t)stream);
 }
 
+sfa_status sfa_attn_fwd_blocksel(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val,
+                                 const uint8_t *k_idx, const void *k_val, const void *v, const int32_t *block_sel,
+                                 int32_t max_sel, void *o, float *lse, void *workspace, size_t workspace_bytes,
+                                 sfa_stream_t stream) {
+    sfa_status s = validate_desc(desc);
+    if (s != SFA_OK) return s;
+    if (desc->dtype != SFA_BF16 || desc->d_v != 128 || (desc->H / desc->H_kv) % 2 != 0 || desc->edges_only ||
+        desc->window > 0 || resolve_kernel(desc) != SFA_KERNEL_SM100_OT)
+        return SFA_ERR_UNSUPPORTED;
+    if (!q_idx || !q_val || !k_idx || !k_val || !v || !o || !lse || !workspace || !block_sel || max_sel < 1)
+        return SFA_ERR_INVALID_ARGUMENT;
+    if (!aligned16(v) || !aligned16(o) || ((uintptr_t)lse & 3u) || !aligned16(workspace) ||
+        ((uintptr_t)block_sel & 3u) || !codes_aligned(q_idx, q_val) || !codes_aligned(k_idx, k_val))
+        return SFA_ERR_INVALID_ARGUMENT;
+    if (workspace_bytes < ws_bytes(desc)) return SFA_ERR_RESOURCE;
+    cudaStream_t st = (cudaStream_t)stream;
+    s = run_prepare(desc, k_idx, k_val, v, workspace, st);
+    if (s != SFA_OK) return s;
+    AttnParams p = make_params(desc, q_idx, q_val, k_idx, k_val, v, o, lse, workspace);
+    p.bsel = block_sel;
+    p.max_sel = max_sel;
+    return from_launch(launch_attn_sm100_ot(p, desc->d, desc->d_v, st, nullptr));
+}
+
 sfa_status sfa_attn_fwd_fused_q(const sfa_attn_desc *desc, const void *q, const uint8_t *k_idx, const void *k_val,
                                 const void *v, void *o, float *lse, uint8_t *q_idx_out, void *q_val_out,
                                 uint32_t *status_word, const void *workspace, size_t workspace_bytes,

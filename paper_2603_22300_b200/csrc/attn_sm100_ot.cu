@@ -170,12 +170,16 @@ __device__ __forceinline__ void decode_item(const OtArgs &a, int item, int &b, T
     }
 }
 
-// one work item's geometry: batch, kv group, its key tiles j0, j0 + 1, ..., j0 + nt - 1
+// one work item's geometry: batch, kv group, its key tiles j0, j0 + 1, ..., j0 + nt - 1 -- or, with a
+// block selection (BSEL, NSA-style token sparsity), the tiles bl[0 .. nt) (none: no selected tile at or
+// below the causal limit -> one fully masked tile, O = 0, LSE = -inf)
 struct ItemGeo {
     int b, g, nt, j0;
     Tile tl[2];
+    const int32_t *bl;
+    bool none;
 };
-template <bool WIN>
+template <bool WIN, bool BSEL = false>
 __device__ __forceinline__ ItemGeo item_geo(const OtArgs &a, int item) {
     const AttnParams &p = a.p;
     ItemGeo G;
@@ -197,9 +201,27 @@ __device__ __forceinline__ ItemGeo item_geo(const OtArgs &a, int item) {
         if (j0 > nt - 1) j0 = nt - 1;  // no key left: one fully masked tile (O = 0, LSE = -inf)
         nt -= j0;
     }
+    G.bl = nullptr;
+    G.none = false;
+    if (BSEL) {  // the selected key tiles of the item's query block (both tiles share it: pair_heads)
+        G.bl = p.bsel + ((int64_t)(G.b * p.H_kv + G.g) * a.nqb + G.tl[0].qb) * p.max_sel;
+        int cnt = 0;
+        while (cnt < p.max_sel) {
+            const int t = __ldg(G.bl + cnt);
+            if (t < 0 || t >= nt) break;  // ascending list: the rest is padding or above the causal limit
+            ++cnt;
+        }
+        G.none = cnt == 0;
+        nt = cnt > 0 ? cnt : 1;
+    }
     G.nt = nt;
     G.j0 = j0;
     return G;
+}
+// the key tile of iteration j of an item
+template <bool BSEL>
+__device__ __forceinline__ int key_tile(const ItemGeo &G, int j) {
+    return BSEL ? (G.none ? 0 : __ldg(G.bl + j)) : G.j0 + j;
 }
 // the m-th work item of this CTA (-1: none left), from the ring the K~ producer fills; every consumer
 // warp reads each slot once and releases it (one arrive per warp; single-lane roles call with
@@ -239,7 +261,9 @@ __device__ __forceinline__ void prefetch_l1(const void *ptr) {
 // (topk_row.cuh), writes the masked row straight into the swizzled Q~ tile and (optionally) the row's
 // code to q_idx_out / q_val_out; the decompression warps then only build K~.
 // WIN: causal sliding window (N4) -- a template flag so the full-causal kernel carries none of its work.
-template <int D, bool DBG, bool EDGE, bool FUSEQ, bool WIN>
+// BSEL: NSA-style block selection (N4): per (b, kv head, query block) an ascending list of the key tiles
+// the block may attend (p.bsel), intersected with the causal mask; EDGE / FUSEQ / WIN off.
+template <int D, bool DBG, bool EDGE, bool FUSEQ, bool WIN, bool BSEL>
 __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid_constant__ CUtensorMap tmap_v,
                                                                       const __grid_constant__ CUtensorMap tmap_k,
                                                                       const OtArgs a) {
@@ -260,7 +284,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
     for (int m_ = 0;; ++m_) {                                                                      \
         const int item_ = ring_get(ring, BAR(IFULL), BAR(IEMPTY), m_, WHOLE_WARP);                 \
         if (item_ < 0) break;                                                                      \
-        const ItemGeo G_ = item_geo<WIN>(a, item_);                                                \
+        const ItemGeo G_ = item_geo<WIN, BSEL>(a, item_);                                                \
         const int b = G_.b, g = G_.g, nt = G_.nt, j0 = G_.j0;                                      \
         const Tile tl[2] = {G_.tl[0], G_.tl[1]};                                                   \
         (void)b; (void)g; (void)tl;
@@ -401,16 +425,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         if (EDGE && lane < 2 * (D / 16)) prefetch_l1(kf_head + lane * 8);  // tile 0: D x 16 bytes of bitsets
         float m = -INFINITY, l = 0.f;
         for (int j = 0; j < nt; ++j) {
-            int64_t lim64 = kend - (int64_t)(j0 + j) * BN;
+            const int kt = key_tile<BSEL>(G_, j);
+            int64_t lim64 = (BSEL && G_.none) ? 0 : kend - (int64_t)kt * BN;
             const int lim = lim64 < 0 ? 0 : (lim64 > BN ? BN : (int)lim64);
             int lo = 0;  // first allowed key of the window in this tile
             if (WIN) {
-                const int64_t lo64 = kbeg - (int64_t)(j0 + j) * BN;
+                const int64_t lo64 = kbeg - (int64_t)kt * BN;
                 lo = lo64 < 0 ? 0 : (lo64 > BN ? BN : (int)lo64);
             }
             uint32_t eh[4];
             if (EDGE) {
-                const uint4 *kf = kf_head + (int64_t)(j0 + j) * D;
+                const uint4 *kf = kf_head + (int64_t)kt * D;
                 uint4 h = make_uint4(0u, 0u, 0u, 0u);
                 if (row_ok && p.k <= 16) {
 #pragma unroll
@@ -675,7 +700,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                 };
                 int m = 0, item = ring_get(ring, BAR(IFULL), BAR(IEMPTY), 0, false);
                 if (item >= 0) {
-                    ItemGeo G = item_geo<WIN>(a, item);
+                    ItemGeo G = item_geo<WIN, BSEL>(a, item);
                     mbar_wait(BAR(QFULL), 0);
                     next_S(G.nt == 1);
                     for (;;) {
@@ -688,7 +713,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                                 // the K~ producer publishes the next item after this item's last K~ load
                                 item_n = ring_get(ring, BAR(IFULL), BAR(IEMPTY), m + 1, false);
                                 if (item_n >= 0) {
-                                    Gn = item_geo<WIN>(a, item_n);
+                                    Gn = item_geo<WIN, BSEL>(a, item_n);
                                     mbar_wait(BAR(QFULL), (m + 1) & 1);
                                     next_S(Gn.nt == 1);
                                 }
@@ -724,7 +749,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                     const uint32_t dst = sbase + C::OFF_V + vs * C::VT;
 #pragma unroll
                     for (int cb = 0; cb < DV / 64; ++cb)
-                        tma_load_3d(dst + cb * BN * 128, &tmap_v, BAR(VFULL + vs), cb * 64, (j0 + j) * BN, bhkv);
+                        tma_load_3d(dst + cb * BN * 128, &tmap_v, BAR(VFULL + vs), cb * 64, key_tile<BSEL>(G_, j) * BN, bhkv);
                 }
                 ITEM_LOOP_END
             }
@@ -742,7 +767,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                     ring[slot] = item_;
                     mbar_arrive(BAR(IFULL + slot));
                     if (item_ < 0) break;
-                    const ItemGeo G_ = item_geo<WIN>(a, item_);
+                    const ItemGeo G_ = item_geo<WIN, BSEL>(a, item_);
                     const int b = G_.b, g = G_.g, nt = G_.nt, j0 = G_.j0;
                 const int bhkv = b * p.H_kv + g;
                 for (int j = 0; j < nt; ++j, ++kc) {
@@ -752,7 +777,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                     const uint32_t dst = sbase + C::OFF_K + s * C::KT;
 #pragma unroll
                     for (int cb = 0; cb < D / 64; ++cb)
-                        tma_load_3d(dst + cb * BN * 128, &tmap_k, BAR(KFULL + s), cb * 64, (j0 + j) * BN, bhkv);
+                        tma_load_3d(dst + cb * BN * 128, &tmap_k, BAR(KFULL + s), cb * 64, key_tile<BSEL>(G_, j) * BN, bhkv);
                 }
                 ITEM_LOOP_END
             }
@@ -811,13 +836,14 @@ cudaError_t launch_t(const OtArgs &a, cudaStream_t stream, int items) {
         if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
     }
     const bool win = p.window > 0;
-    auto kern = p.q_dense != nullptr ? attn_sm100_ot_kernel<D, false, false, true, false>
-                : win ? (p.edges_only ? attn_sm100_ot_kernel<D, false, true, false, true>
-                                      : attn_sm100_ot_kernel<D, false, false, false, true>)
-                : p.edges_only ? (a.dbg != nullptr ? attn_sm100_ot_kernel<D, true, true, false, false>
-                                                   : attn_sm100_ot_kernel<D, false, true, false, false>)
-                               : (a.dbg != nullptr ? attn_sm100_ot_kernel<D, true, false, false, false>
-                                                   : attn_sm100_ot_kernel<D, false, false, false, false>);
+    auto kern = p.bsel != nullptr ? attn_sm100_ot_kernel<D, false, false, false, false, true>
+                : p.q_dense != nullptr ? attn_sm100_ot_kernel<D, false, false, true, false, false>
+                : win ? (p.edges_only ? attn_sm100_ot_kernel<D, false, true, false, true, false>
+                                      : attn_sm100_ot_kernel<D, false, false, false, true, false>)
+                : p.edges_only ? (a.dbg != nullptr ? attn_sm100_ot_kernel<D, true, true, false, false, false>
+                                                   : attn_sm100_ot_kernel<D, false, true, false, false, false>)
+                               : (a.dbg != nullptr ? attn_sm100_ot_kernel<D, true, false, false, false, false>
+                                                   : attn_sm100_ot_kernel<D, false, false, false, false, false>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     // persistent: one CTA per SM takes items from the work counter; the fused-Q prologue keeps one item
@@ -843,6 +869,10 @@ cudaError_t launch_attn_sm100_ot(const AttnParams &p, int d, int d_v, cudaStream
     if (p.edges_only && p.kfmask == nullptr) return cudaErrorInvalidValue;
     if (p.q_dense != nullptr && (p.edges_only || dbg != nullptr || p.window > 0)) return cudaErrorNotSupported;
     if (p.window > 0 && dbg != nullptr) return cudaErrorNotSupported;
+    // block selection: R1, no window, no fused Q; both tiles of an item must share the query block
+    if (p.bsel != nullptr && (p.edges_only || p.window > 0 || p.q_dense != nullptr || dbg != nullptr ||
+                              (p.H / p.H_kv) % 2 != 0 || p.max_sel < 1))
+        return cudaErrorNotSupported;
     OtArgs a;
     a.p = p;
     a.nqb = (int)((p.n_q + BM - 1) / BM);

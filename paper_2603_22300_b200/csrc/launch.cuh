@@ -14,6 +14,9 @@ struct AttnParams {
     const uint32_t *v_amax;  // sm100: per (b, kv head) max|V| bits, e = vprep_head_exp(bits)
     const void *k_dense = nullptr;  // SM100_OT: decompressed K~ rows, bf16 [B][H_kv][n_kv][d] (vprep.cu)
     uint32_t *sched = nullptr;      // SM100_OT: the persistent tile scheduler's work counter (workspace)
+    // N4 block selection (SM100_OT): [B][H_kv][ceil(n_q/128)][max_sel] ascending key-tile indices, -1 padded
+    const int32_t *bsel = nullptr;
+    int32_t max_sel = 0;
     void *o;
     float *lse;
     const uint8_t *ws;

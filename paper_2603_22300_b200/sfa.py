@@ -83,6 +83,7 @@ def lib() -> ctypes.CDLL:
             "sfa_attn_bwd_workspace_bytes": ([D], SZ),
             "sfa_attn_bwd": ([D, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P], I32),
             "sfa_attn_fwd_fused_q": ([D, P, P, P, P, P, P, P, P, P, P, SZ, P], I32),
+            "sfa_attn_fwd_blocksel": ([D, P, P, P, P, P, P, I32, P, P, P, SZ, P], I32),
             "sfa_dist_kv_plan": ([D, I32, ctypes.POINTER(KvPlan)], I32),
             "sfa_dist_zigzag_chunk": ([I64, I32, I32, I32, ctypes.POINTER(I64), ctypes.POINTER(I64)], I32),
             "sfa_dist_head_shard": ([D, I32, I32, D, ctypes.POINTER(I64)], I32),
@@ -99,7 +100,7 @@ EXPORTS = ("sfa_status_string", "sfa_topk_codes", "sfa_topk_codes_qk", "sfa_attn
            "sfa_forward_host", "sfa_device_supported", "sfa_gen_fill", "sfa_debug_sm100_scores",
            "sfa_attn_prepare", "sfa_attn_fwd_prepared", "sfa_dist_unique_id", "sfa_dist_init", "sfa_dist_destroy",
            "sfa_dist_staging_bytes", "sfa_dist_allgather_kv", "sfa_dist_unpack_zigzag", "sfa_forward_host_pipelined",
-           "sfa_attn_bwd_workspace_bytes", "sfa_attn_bwd", "sfa_attn_fwd_fused_q", "sfa_dist_kv_plan",
+           "sfa_attn_bwd_workspace_bytes", "sfa_attn_bwd", "sfa_attn_fwd_fused_q", "sfa_attn_fwd_blocksel", "sfa_dist_kv_plan",
            "sfa_dist_zigzag_chunk", "sfa_dist_head_shard")
 
 
@@ -245,6 +246,30 @@ def attn_fwd(q_idx, q_val, k_idx, k_val, v, *, d, causal=True, scale=None, q_pos
         o, lse = out
     _check(lib().sfa_attn_fwd(ctypes.byref(desc), _p(q_idx), _p(q_val), _p(k_idx), _p(k_val), _p(v), _p(o),
                               _p(lse), _p(workspace), workspace.numel(), _stream()), "sfa_attn_fwd")
+    return o, lse
+
+
+def attn_fwd_blocksel(q_idx, q_val, k_idx, k_val, v, block_sel, *, d, causal=True, scale=None, q_pos0=0,
+                      workspace=None):
+    """Stage 2 composed with NSA-style block selection (sfa_attn_fwd_blocksel):
+    block_sel int32 [B, H_kv, ceil(n_q/128), max_sel], ascending key-block indices padded with -1."""
+    _dev(q_idx, q_val, k_idx, k_val, v, block_sel)
+    _check_codes(q_idx, q_val, k_idx, k_val, v, d)
+    B, H, n_q, _ = q_idx.shape
+    H_kv = k_idx.shape[1]
+    if block_sel.dtype != torch.int32 or block_sel.dim() != 4 or not block_sel.is_contiguous() or \
+            tuple(block_sel.shape[:3]) != (B, H_kv, (n_q + 127) // 128):
+        raise ValueError("block_sel: contiguous int32 [B, H_kv, ceil(n_q/128), max_sel]")
+    desc = _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, KERNEL_AUTO, _dt(v))
+    nb = workspace_bytes(desc)
+    if workspace is None:
+        workspace = torch.empty(max(nb, 16), dtype=torch.uint8, device=v.device)
+    _check_ws(workspace, nb)
+    o = torch.empty((B, H, n_q, v.shape[-1]), dtype=v.dtype, device=v.device)
+    lse = torch.empty((B, H, n_q), dtype=torch.float32, device=v.device)
+    _check(lib().sfa_attn_fwd_blocksel(ctypes.byref(desc), _p(q_idx), _p(q_val), _p(k_idx), _p(k_val), _p(v),
+                                       _p(block_sel), int(block_sel.shape[3]), _p(o), _p(lse), _p(workspace),
+                                       workspace.numel(), _stream()), "sfa_attn_fwd_blocksel")
     return o, lse
 
 

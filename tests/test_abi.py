@@ -128,6 +128,15 @@ def test_n4_semantics_validation(sfa):
     for b in (dict(window=-1), dict(window=16, causal=False)):
         d = desc(sfa, **b)
         assert L.sfa_attn_fwd(ctypes.byref(d), *([ctypes.c_void_p(16)] * 8), 1 << 30, None) == 1, b
+    # block selection (N4): argument and support checks before any launch
+    bsf = L.sfa_attn_fwd_blocksel
+    dv16 = ctypes.c_void_p(16)
+    assert bsf(ctypes.byref(desc(sfa)), *([dv16] * 6), 0, dv16, dv16, dv16, 1 << 30, None) == 1        # max_sel 0
+    assert bsf(ctypes.byref(desc(sfa)), *([dv16] * 5), None, 4, dv16, dv16, dv16, 1 << 30, None) == 1   # no list
+    for b in (dict(H=6, H_kv=2), dict(edges_only=True), dict(window=64), dict(d_v=64),
+              dict(dtype=sfa.SFA_F32), dict(kernel=sfa.KERNEL_SM100_PP)):
+        assert bsf(ctypes.byref(desc(sfa, **b)), *([dv16] * 6), 4, dv16, dv16, dv16, 1 << 30, None) == 3, b
+    assert bsf(ctypes.byref(desc(sfa)), *([dv16] * 6), 4, dv16, dv16, dv16, 16, None) == 4             # workspace
     # the round-1 ablation kernels PAIR / WIDE were removed in round 2: their numbers stay reserved
     for kern in (sfa.KERNEL_SM100_PAIR, sfa.KERNEL_SM100_WIDE):
         assert L.sfa_attn_fwd(ctypes.byref(desc(sfa, kernel=kern)), *([ctypes.c_void_p(16)] * 8), 1 << 30, None) == 3
