@@ -56,7 +56,7 @@ typedef enum { SFA_F32 = 0, SFA_BF16 = 1 } sfa_dtype;
 /* Kernel selection for sfa_attn_fwd (desc.kernel). */
 typedef enum {
     SFA_KERNEL_AUTO = 0, /* SIMT for fp32; for bf16 DECODE when n_q * H / H_kv <= 16, else SM100_OT for
-                            d_v = 128 and SM100 for d_v = 64                                           */
+                            d_v = 128 and SM100 for d_v = 64; bf16 with edges_only or a window: SM100_OT */
     SFA_KERNEL_SIMT = 1, /* CUDA-core kernel: key-tile feature buckets, shared-memory scatter of the
                             support overlaps, FFMA P.V (the only fp32 path: reading A12)             */
     SFA_KERNEL_SM100 = 2, /* sm_100a kernel (bf16 only): key codes decompressed on chip, S = Q~ K~^T and
@@ -67,7 +67,8 @@ typedef enum {
                                   CUDA-core kernel reading codes + V, LSE merge.  AUTO picks
                                   it for such shapes.                                                      */
     SFA_KERNEL_SM100_OT = 6,   /* SM100 with a transposed output accumulator: O^T += V^T P^T as N = 256 MMAs
-                                  over both query tiles, P in shared memory (bf16, d_v = 128)              */
+                                  over both query tiles, P in shared memory (bf16; d_v = 64 runs the same
+                                  d_v = 128 product over V's zero-padded fp16 copy)                        */
     SFA_KERNEL_SM100_PP = 7,   /* two query tiles in ping-pong: K~ tiles by TMA from key rows decompressed
                                   once per key (prepare step), P in TMEM (TS-MMA P.V), exponential phases
                                   of the two softmax warpgroups alternating (bf16, R1, no window)          */
@@ -118,8 +119,8 @@ typedef struct {
                             to softmax(Q~K~^T/sqrt d)V").  1: R2 -- only the "nonzero
                             attention edges": pair (i, j) enters iff the supports share
                             a feature index (zero-valued selected entries count, A8); a row with no edge
-                            gets O = 0, LSE = -inf.  R2 runs on SM100_OT (bf16, d_v = 128) and SIMT
-                            (AUTO picks them); other explicit kernels -> SFA_ERR_UNSUPPORTED.          */
+                            gets O = 0, LSE = -inf.  R2 runs on SM100_OT (bf16) and SIMT (AUTO picks
+                            them); other explicit kernels -> SFA_ERR_UNSUPPORTED.                      */
     int64_t window;      /* 0: off.  > 0 (requires causal = 1): causal sliding window -- SFA composed with
                             token-level sparsity: key j is allowed only if
                             also j > q_pos0 + i - window.  Key tiles before a query block's window are

@@ -36,8 +36,7 @@ sfa_status validate_desc(const sfa_attn_desc *d) {
          d->kernel == SFA_KERNEL_SM100_OT || d->kernel == SFA_KERNEL_SM100_PP || d->kernel == SFA_KERNEL_SM100_OTH) &&
         d->dtype != SFA_BF16)
         return SFA_ERR_UNSUPPORTED;
-    if ((d->kernel == SFA_KERNEL_SM100_PAIR || d->kernel == SFA_KERNEL_SM100_OT || d->kernel == SFA_KERNEL_SM100_OTH) &&
-        d->d_v != 128)
+    if ((d->kernel == SFA_KERNEL_SM100_PAIR || d->kernel == SFA_KERNEL_SM100_OTH) && d->d_v != 128)
         return SFA_ERR_UNSUPPORTED;
     if (d->kernel == SFA_KERNEL_DECODE &&
         (d->dtype != SFA_BF16 || (int64_t)(d->H / d->H_kv) * d->n_q > 16))
@@ -65,11 +64,13 @@ BucketLayout layout_of(const sfa_attn_desc *d) {
 
 // Which attention kernel a desc runs.  AUTO: the CUDA-core kernel for fp32 (reading A12); for bf16
 // the split-KV decode kernel when a kv head has at most 16 query rows (n_q * H / H_kv), else the
-// sm_100a tensor-core kernel: the transposed-output one (SM100_OT) for d_v = 128, SM100 for d_v = 64.
+// sm_100a tensor-core kernel: the transposed-output one (SM100_OT) for d_v = 128, SM100 for d_v = 64 (at the
+// GPT-2 shape SM100 is faster: 0.054 vs 0.070 ms, profiles/r02_gpt2_ot_dv64.txt), except that R2 and the
+// sliding window are built into SM100_OT only (d_v = 64 over the zero-padded V copy).
 int resolve_kernel(const sfa_attn_desc *d) {
     if (d->kernel == SFA_KERNEL_SIMT || d->dtype == SFA_F32) return SFA_KERNEL_SIMT;
     if (d->kernel != SFA_KERNEL_AUTO) return d->kernel;
-    if (d->edges_only || d->window > 0) return d->d_v == 128 ? SFA_KERNEL_SM100_OT : SFA_KERNEL_SIMT;  // R2 / window
+    if (d->edges_only || d->window > 0) return SFA_KERNEL_SM100_OT;  // R2 / window: built into SM100_OT only
     if ((int64_t)(d->H / d->H_kv) * d->n_q <= 16) return SFA_KERNEL_DECODE;
     return d->d_v == 128 ? SFA_KERNEL_SM100_OT : SFA_KERNEL_SM100;
 }
@@ -83,8 +84,10 @@ size_t bucket_bytes(const sfa_attn_desc *d) {
 // sm100 workspace: [max|V| per (b, kv head), 256-aligned][fp16 copy of V scaled by 2^-e] (vprep.cu);
 // the sm100 kernel decompresses key codes on chip and needs no buckets
 size_t vprep_amax_bytes(const sfa_attn_desc *d) { return align_up((int64_t)d->B * d->H_kv * 4, 256); }
+// features per row of the fp16 V copy: SM100_OT's P.V is d_v = 128 wide, so a d_v = 64 head is padded
+int v16_cols(const sfa_attn_desc *d) { return resolve_kernel(d) == SFA_KERNEL_SM100_OT ? 128 : d->d_v; }
 size_t vprep_bytes(const sfa_attn_desc *d) {
-    return vprep_amax_bytes(d) + (size_t)d->B * d->H_kv * d->n_kv * d->d_v * 2;
+    return vprep_amax_bytes(d) + (size_t)d->B * d->H_kv * d->n_kv * v16_cols(d) * 2;
 }
 // SM100_OT: the decompressed K~ rows (bf16, read by TMA) follow the V prep, 256-aligned; then, for R2,
 // the key-tile feature bitsets (edges.cu)
@@ -164,9 +167,17 @@ sfa_status run_prepare(const sfa_attn_desc *d, const uint8_t *k_idx, const void 
     if (uses_simt(d))
         return from_cuda(launch_bucket(k_idx, k_val, d->dtype == SFA_BF16, d->d, d->k, (int64_t)d->B * d->H_kv,
                                        d->n_kv, p.L, ws, st));
-    cudaError_t e = launch_vprep(v, (int64_t)d->B * d->H_kv, d->n_kv, d->d_v, (uint32_t *)p.v_amax, (void *)p.v16, st);
-    if (e == cudaSuccess && uses_kdense(d))
-        e = launch_kdense(k_idx, k_val, (int64_t)d->B * d->H_kv * d->n_kv, d->d, d->k, (void *)p.k_dense, st);
+    const int64_t bh_kv = (int64_t)d->B * d->H_kv;
+    cudaError_t e;
+    if (prep_small_ok(bh_kv, d->n_kv, d->d_v, uses_kdense(d) ? bh_kv * d->n_kv : 0)) {
+        // small heads: max|V|, the fp16 V copy and the K~ rows in one launch
+        e = launch_prep_small(v, bh_kv, d->n_kv, d->d_v, v16_cols(d), (uint32_t *)p.v_amax, (void *)p.v16, k_idx, k_val,
+                              d->d, d->k, uses_kdense(d) ? (void *)p.k_dense : nullptr, st);
+    } else {
+        e = launch_vprep(v, bh_kv, d->n_kv, d->d_v, v16_cols(d), (uint32_t *)p.v_amax, (void *)p.v16, st);
+        if (e == cudaSuccess && uses_kdense(d))
+            e = launch_kdense(k_idx, k_val, bh_kv * d->n_kv, d->d, d->k, (void *)p.k_dense, st);
+    }
     if (e == cudaSuccess && uses_kmask(d))
         e = launch_kfmask(k_idx, (int64_t)d->B * d->H_kv, d->n_kv, d->d, d->k, (uint32_t *)p.kfmask, st);
     return from_cuda(e);

@@ -106,6 +106,7 @@ struct OtArgs {
     int32_t per_rank;    // work items per q-block rank
     int32_t nkt;         // ceil(n_kv / BN)
     int32_t items;       // work items (the persistent CTAs walk them, sched_item)
+    int32_t dv_out;      // d_v of O (64: V's fp16 copy is zero-padded to DV = 128 columns, vprep.cu)
     float c_scale;       // scale * log2(e)
     float *dbg;          // optional: raw S of the first key tile of work item 0, tile 0 (tests)
 };
@@ -630,9 +631,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         named_bar_sync(bar_id, 128);
         const int64_t orow = ((int64_t)b * p.H + tl[t].h) * p.n_q + i;
         if (row_ok) {
-            uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<uint16_t *>(p.o) + orow * DV);
+            uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<uint16_t *>(p.o) + orow * a.dv_out);
+            if (a.dv_out == DV) {
 #pragma unroll
-            for (int c = 0; c < DV / 8; ++c) dst[c] = lds_v4(so + (uint32_t)r * (DV * 2) + ((uint32_t)(c ^ (r & 15)) << 4));
+                for (int c = 0; c < DV / 8; ++c) dst[c] = lds_v4(so + (uint32_t)r * (DV * 2) + ((uint32_t)(c ^ (r & 15)) << 4));
+            } else {  // d_v = 64: the padded features 64..127 of O^T are zero and not stored
+#pragma unroll
+                for (int c = 0; c < DV / 16; ++c) dst[c] = lds_v4(so + (uint32_t)r * (DV * 2) + ((uint32_t)(c ^ (r & 15)) << 4));
+            }
             p.lse[orow] = l > 0.f ? (m + __log2f(l) - P_SHIFT) * 0.69314718055994530942f : -INFINITY;
         }
         // both tiles' staging (the dead P buffer, where the other tile's rows interleave) is read before
@@ -865,7 +871,9 @@ cudaError_t launch_t(const OtArgs &a, cudaStream_t stream, int items) {
 }  // namespace
 
 cudaError_t launch_attn_sm100_ot(const AttnParams &p, int d, int d_v, cudaStream_t stream, float *dbg) {
-    if ((d != 64 && d != 128) || d_v != DV) return cudaErrorNotSupported;
+    // d_v = 64 runs the same kernel over V's fp16 copy zero-padded to DV = 128 columns (vprep.cu): the
+    // extra half of the P.V is free next to the fixed costs of the small heads that have d_v = 64
+    if ((d != 64 && d != 128) || (d_v != DV && d_v != 64)) return cudaErrorNotSupported;
     if (p.edges_only && p.kfmask == nullptr) return cudaErrorInvalidValue;
     if (p.q_dense != nullptr && (p.edges_only || dbg != nullptr || p.window > 0)) return cudaErrorNotSupported;
     if (p.window > 0 && dbg != nullptr) return cudaErrorNotSupported;
@@ -882,6 +890,7 @@ cudaError_t launch_attn_sm100_ot(const AttnParams &p, int d, int d_v, cudaStream
     a.c_scale *= 1.f + 1.f / 512.f;
 #endif
     a.dbg = dbg;
+    a.dv_out = d_v;
     const int R = p.H / p.H_kv;
     a.pair_heads = (R % 2 == 0) ? 1 : 0;
     int64_t items;

@@ -48,9 +48,15 @@ cudaError_t launch_topk_pair(const void *x0, int64_t rows0, int64_t ld0, uint8_t
                              uint32_t *status_word, cudaStream_t stream);
 cudaError_t launch_bucket(const uint8_t *k_idx, const void *k_val, bool bf16, int d, int k, int64_t bh_kv,
                           int64_t n_kv, const BucketLayout &L, void *ws, cudaStream_t stream);
-// P.V operand prep for the sm100 kernel: amax[bh] = max|V| bits, v16 = fp16(V * 2^-e) (vprep.cu)
-cudaError_t launch_vprep(const void *v, int64_t bh_kv, int64_t n_kv, int d_v, uint32_t *amax, void *v16,
+// P.V operand prep for the sm100 kernel: amax[bh] = max|V| bits, v16 = fp16(V * 2^-e) (vprep.cu), rows of
+// dvp >= d_v features (zeros past d_v)
+cudaError_t launch_vprep(const void *v, int64_t bh_kv, int64_t n_kv, int d_v, int dvp, uint32_t *amax, void *v16,
                          cudaStream_t stream);
+// the same plus the K~ rows (k_dense != null) in ONE launch without a memset, one block per (batch, kv
+// head) (vprep.cu prep_small_kernel): for heads of at most 128 KB of V (prep_small_ok)
+bool prep_small_ok(int64_t bh_kv, int64_t n_kv, int d_v, int64_t krows);
+cudaError_t launch_prep_small(const void *v, int64_t bh_kv, int64_t n_kv, int d_v, int dvp, uint32_t *amax, void *v16,
+                              const uint8_t *k_idx, const void *k_val, int d, int k, void *k_dense, cudaStream_t stream);
 // e with max|V| * 2^-e in [2^14, 2^15) (fp16-safe and clear of fp16's subnormal range, in either
 // direction: small heads are scaled UP), clamped to e >= -126 so that 2^-e and 2^e are both normal
 // floats; e = 0 for an all-zero head.  Shared by vprep.cu and the attention epilogues.

@@ -110,17 +110,21 @@ __global__ void __launch_bounds__(256) topk_codes_kernel(const Bits *__restrict_
 
 // ---------------------------------------------------------------------------------------------
 // bf16 rows: one THREAD per row (the warp-per-row kernel above issues ~500 warp instructions per
-// row and is ALU-bound at ~9% of HBM bandwidth).  A CTA of 128 threads owns 128 consecutive rows:
-//   1. coalesced 16-byte loads of the rows into shared memory, 16-byte chunks XOR-swizzled by
-//      (row & 15) so each thread then reads its own row with conflict-free LDS.128;
-//   2. the row as 64 (d=128) or 32 (d=64) registers of two |bf16| bit patterns each (sign cleared:
-//      for finite non-negative bf16 the numeric order IS the order of the 15-bit keys);
-//   3. the same bitwise binary search for the k-th largest key T (15 steps), counting on the FP16
-//      pipe: set.ge.bf16x2 (1.0 per key >= T) + add.bf16x2 into four exact accumulators, 2
-//      instructions per 2 keys (the integer subtract/popc version kept the ALU pipe at 82 %);
-//   4. selection bit masks (set.ge against T + 1, set.eq against T), ties == T taken lowest index
-//      first (A2), then the set bits walked in ascending feature order (A4) with the values
-//      re-read from the row in shared memory; staged and written out with coalesced stores.
+// row and is ALU-bound at ~9% of HBM bandwidth).  A CTA of 128 threads owns blocks of 128
+// consecutive rows; the grid is persistent (a few CTAs per SM, each walking blocks with a stride of
+// the grid) and double-buffered:
+//   1. the NEXT block's rows stream into the second shared-memory buffer with cp.async (16 bytes per
+//      thread per step, coalesced), 16-byte chunks XOR-swizzled by (row & 15) so each thread then
+//      reads its own row with conflict-free LDS.128, while the current block is selected;
+//   2. the row as D/2 registers in the split layout of topk_row.cuh (word i = |x_i|, |x_{i+D/2}|,
+//      sign cleared: for finite non-negative bf16 the numeric order IS the order of the 15-bit keys);
+//   3. the k-th largest key T: exponent first from the row max, then the mantissa bits, counting on
+//      the FP16 pipe (set.ge.bf16x2 + add.bf16x2, 2 instructions per 2 keys), stopping once every
+//      row of the warp counts exactly k keys >= T;
+//   4. selection bit masks (one set.ge.u32.bf16x2 + one LOP3 per 2 keys), ties == T taken lowest
+//      index first (A2) on the rare rows that have them, then the set bits walked in ascending
+//      feature order (A4) with the values re-read from the row in shared memory; staged and written
+//      out with coalesced stores.
 // Non-finite inputs: max key (max.u16x2) >= 0x7F80.
 constexpr int TK_ROWS = 128;
 
@@ -136,83 +140,178 @@ struct TkSeg {
 struct TkSegs {
     TkSeg s[2];
     int64_t nb0;  // blocks of segment 0
+    int64_t nb;   // blocks of both segments
 };
 
-template <int D>
-__global__ void __launch_bounds__(TK_ROWS) topk_rows_bf16_kernel(const __grid_constant__ TkSegs segs, int k,
-                                                                 uint32_t *status_word) {
-    constexpr int NW = D / 2;     // u32 words per row
-    constexpr int NC = D / 8;     // 16-byte chunks per row
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
+}
+
+// KC = k when k is 8 or 16 (compile time: the row's code is assembled in registers and stored with
+// 16-byte stores straight to global, coalesced across the warp's consecutive rows), else 0 (runtime k:
+// staged in shared memory and copied out per block)
+template <int D, int KC>
+__global__ void __launch_bounds__(TK_ROWS, 3) topk_rows_bf16_kernel(const __grid_constant__ TkSegs segs, int k,
+                                                                    uint32_t *status_word) {
+    constexpr int NW = D / 2;            // u32 words per row
+    constexpr int NC = D / 8;            // 16-byte chunks per row
+    constexpr int NM = D / 32;           // selection mask words
+    constexpr int RB = TK_ROWS * D * 2;  // bytes of one row buffer
+    constexpr int RPI = TK_ROWS / NC;    // rows per cp.async step of the CTA
     extern __shared__ __align__(16) uint8_t sm[];
-    uint8_t *rowbuf = sm;                                   // [TK_ROWS][D*2] swizzled
-    uint8_t *oidx = sm + TK_ROWS * D * 2;                   // [TK_ROWS][k]
-    uint16_t *oval = reinterpret_cast<uint16_t *>(oidx + ((TK_ROWS * k + 15) & ~15));  // [TK_ROWS][k]
+    uint8_t *oidx = sm + 2 * RB;                                                       // KC = 0: [TK_ROWS][k]
+    uint16_t *oval = reinterpret_cast<uint16_t *>(oidx + ((TK_ROWS * k + 15) & ~15));  // KC = 0: [TK_ROWS][k]
     const int t = threadIdx.x;
-    const bool second = (int64_t)blockIdx.x >= segs.nb0;
-    const TkSeg &sg = second ? segs.s[1] : segs.s[0];
-    const uint16_t *__restrict__ x = sg.x;
-    const int64_t rows = sg.rows, ld = sg.ld;
-    uint8_t *__restrict__ idx = sg.idx;
-    uint16_t *__restrict__ val = sg.val;
-    const int64_t row0 = ((int64_t)blockIdx.x - (second ? segs.nb0 : 0)) * TK_ROWS;
-    const int nrows = (int)((rows - row0) < TK_ROWS ? (rows - row0) : TK_ROWS);
+    const int cc = t % NC, r0 = t / NC;  // this thread's 16-byte chunk column and first row of every copy
 
-    // 1. coalesced loads (16 B per thread per step), swizzled stores
-    for (int v = t; v < nrows * NC; v += TK_ROWS) {
-        const int r = v / NC, c = v % NC;
-        const uint4 w = __ldcs(reinterpret_cast<const uint4 *>(x + (row0 + r) * ld) + c);
-        *reinterpret_cast<uint4 *>(rowbuf + r * D * 2 + ((c ^ (r & 15) & (NC - 1)) << 4)) = w;
-    }
-    __syncthreads();
-
-    const bool active = t < nrows;
-    uint32_t ab[NW];  // |x| bit patterns, two keys per word
+    // block b -> (segment, first row, rows in it)
+    auto locate = [&](int64_t b, int64_t &row0, int &nrows) -> const TkSeg & {
+        const bool second = b >= segs.nb0;
+        const TkSeg &sg = second ? segs.s[1] : segs.s[0];
+        row0 = (b - (second ? segs.nb0 : 0)) * TK_ROWS;
+        nrows = (int)((sg.rows - row0) < TK_ROWS ? (sg.rows - row0) : TK_ROWS);
+        return sg;
+    };
+    auto issue = [&](int64_t b, int buf) {
+        int64_t row0;
+        int nrows;
+        const TkSeg &sg = locate(b, row0, nrows);
+        const uint32_t base = (uint32_t)__cvta_generic_to_shared(sm + buf * RB) + (uint32_t)r0 * (D * 2);
+        const char *src = reinterpret_cast<const char *>(sg.x + (row0 + r0) * sg.ld + cc * 8);
+        const int64_t step = (int64_t)RPI * sg.ld * 2;  // bytes between this thread's consecutive rows
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        const uint4 w = *reinterpret_cast<const uint4 *>(rowbuf + t * D * 2 + ((c ^ (t & 15) & (NC - 1)) << 4));
-        ab[4 * c + 0] = w.x & 0x7FFF7FFFu;
-        ab[4 * c + 1] = w.y & 0x7FFF7FFFu;
-        ab[4 * c + 2] = w.z & 0x7FFF7FFFu;
-        ab[4 * c + 3] = w.w & 0x7FFF7FFFu;
-    }
-    const uint32_t mx = tk::row_max_key(ab);
-    if (active && mx >= 0x7F80u && status_word != nullptr) atomicOr(status_word, 1u);
-    // 3-4. threshold search and selection masks (topk_row.cuh)
-    constexpr int NM = D / 32;
-    uint32_t gm[NM];
-    tk::select_masks(ab, k, gm, mx);
-    // 5. ascending compaction into the staging area (values re-read from the row in shared memory)
-    uint8_t *my_i = oidx + t * k;
-    uint16_t *my_v = oval + t * k;
-    int pos = 0;
-#pragma unroll
-    for (int w = 0; w < NM; ++w) {
-        uint32_t m = active ? gm[w] : 0u;
-        while (m != 0u) {
-            const int f = 32 * w + (__ffs(m) - 1);
-            m &= m - 1u;
-            const int c = f >> 3;
-            my_i[pos] = (uint8_t)f;
-            my_v[pos] = *reinterpret_cast<const uint16_t *>(rowbuf + t * D * 2 + ((c ^ (t & 15) & (NC - 1)) << 4) + (f & 7) * 2);
-            ++pos;
+        for (int i = 0; i < NC; ++i, src += step) {
+            const int r = r0 + i * RPI;
+            if (r < nrows)
+                cp_async16(base + (uint32_t)(i * RPI * D * 2) + ((uint32_t)(cc ^ (r & 15) & (NC - 1)) << 4), src);
         }
-    }
-    __syncthreads();
-    // coalesced copy-out of the CTA's contiguous [nrows][k] index and value blocks
-    const int nib = nrows * k;
-    uint8_t *gi = idx + row0 * k;
-    uint16_t *gv = val + row0 * k;
-    if ((k & 15) == 0) {
-        for (int v = t; v < nib / 16; v += TK_ROWS)
-            reinterpret_cast<uint4 *>(gi)[v] = reinterpret_cast<const uint4 *>(oidx)[v];
-    } else {
-        for (int v = t; v < nib; v += TK_ROWS) gi[v] = oidx[v];
-    }
-    if ((k & 7) == 0) {
-        for (int v = t; v < nib / 8; v += TK_ROWS)
-            reinterpret_cast<uint4 *>(gv)[v] = reinterpret_cast<const uint4 *>(oval)[v];
-    } else {
-        for (int v = t; v < nib; v += TK_ROWS) gv[v] = oval[v];
+    };
+
+    int64_t b = blockIdx.x;
+    if (b < segs.nb) issue(b, 0);
+    cp_async_commit();
+    for (int buf = 0; b < segs.nb; b += gridDim.x, buf ^= 1) {
+        if (b + gridDim.x < segs.nb) issue(b + gridDim.x, buf ^ 1);
+        cp_async_commit();
+        cp_async_wait1();  // this block's group has landed (the next one may still be in flight)
+        __syncthreads();
+        const uint8_t *rowbuf = sm + buf * RB;
+        const uint32_t myrow = (uint32_t)__cvta_generic_to_shared(rowbuf) + (uint32_t)t * (D * 2);
+        int64_t row0;
+        int nrows;
+        const TkSeg &sg = locate(b, row0, nrows);
+        const bool active = t < nrows;
+
+        uint32_t ab[NW];  // split layout: word i = |x_i| | |x_{i+NW}| << 16
+#pragma unroll
+        for (int c = 0; c < NC / 2; ++c) {
+            const uint4 X = *reinterpret_cast<const uint4 *>(rowbuf + t * D * 2 + ((c ^ (t & 15) & (NC - 1)) << 4));
+            const uint4 Y =
+                *reinterpret_cast<const uint4 *>(rowbuf + t * D * 2 + (((c + NC / 2) ^ (t & 15) & (NC - 1)) << 4));
+            const uint32_t xs[4] = {X.x, X.y, X.z, X.w}, ys[4] = {Y.x, Y.y, Y.z, Y.w};
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                ab[8 * c + 2 * m] = __byte_perm(xs[m], ys[m], 0x5410) & 0x7FFF7FFFu;
+                ab[8 * c + 2 * m + 1] = __byte_perm(xs[m], ys[m], 0x7632) & 0x7FFF7FFFu;
+            }
+        }
+        uint32_t mx = tk::row_max_key(ab);
+        if (mx >= 0x7F80u) {  // non-finite row (A14): flagged; NaN keys clamped to +inf so that every count
+            // below (bf16 compares and byte arithmetic alike) sees the same numbers and the walk terminates
+            if (active && status_word != nullptr) atomicOr(status_word, 1u);
+#pragma unroll
+            for (int i = 0; i < NW; ++i) asm("min.u16x2 %0, %0, %1;" : "+r"(ab[i]) : "r"(0x7F807F80u));
+            mx = 0x7F80u;
+        }
+        auto val_addr = [&](int f) { return myrow + ((uint32_t)((f >> 3) ^ (t & 15) & (NC - 1)) << 4) + (uint32_t)(f & 7) * 2; };
+        if constexpr (KC > 0) {
+            // exactly KC bits are set over q[]: walk them in ascending order through a queue of the mask
+            // words (an empty word is shifted out, at most NM - 1 times per row)
+            uint32_t q[NM];
+            tk::select_masks_split(ab, KC, q, mx);
+            if (!active) {  // a ragged block's idle rows: any KC bits, nothing stored
+                q[0] = (KC >= 32) ? 0xFFFFFFFFu : ((1u << KC) - 1u);
+#pragma unroll
+                for (int w = 1; w < NM; ++w) q[w] = 0u;
+            }
+            int base = 0;
+            uint32_t iw[KC / 4], vw[KC / 2];  // the row's code: KC index bytes, KC bf16 values
+#pragma unroll
+            for (int i = 0; i < KC / 4; ++i) iw[i] = 0u;
+#pragma unroll
+            for (int i = 0; i < KC / 2; ++i) vw[i] = 0u;
+#pragma unroll
+            for (int pos = 0; pos < KC; ++pos) {
+                while (q[0] == 0u && base < D) {
+#pragma unroll
+                    for (int w = 0; w + 1 < NM; ++w) q[w] = q[w + 1];
+                    q[NM - 1] = 0u;
+                    base += 32;
+                }
+                const int f = q[0] != 0u ? base + __ffs(q[0]) - 1 : 0;  // (never 0 bits: never spin)
+                q[0] &= q[0] - 1u;
+                iw[pos >> 2] |= (uint32_t)f << (8 * (pos & 3));
+                vw[pos >> 1] |= lds_u16(val_addr(f)) << (16 * (pos & 1));
+            }
+            if (active) {
+                const int64_t row = row0 + t;
+                if constexpr (KC == 16) {
+                    reinterpret_cast<uint4 *>(sg.idx)[row] = make_uint4(iw[0], iw[1], iw[2], iw[3]);
+                    uint4 *vr = reinterpret_cast<uint4 *>(sg.val) + 2 * row;
+                    vr[0] = make_uint4(vw[0], vw[1], vw[2], vw[3]);
+                    vr[1] = make_uint4(vw[4], vw[5], vw[6], vw[7]);
+                } else {  // KC == 8
+                    reinterpret_cast<uint2 *>(sg.idx)[row] = make_uint2(iw[0], iw[1]);
+                    reinterpret_cast<uint4 *>(sg.val)[row] = make_uint4(vw[0], vw[1], vw[2], vw[3]);
+                }
+            }
+            // every thread's reads of this row buffer precede the next iteration's cp.async into it
+            __syncthreads();
+        } else {
+            uint32_t gm[NM];
+            tk::select_masks_split(ab, k, gm, mx);
+            // ascending compaction into the staging area (values re-read from the row in shared memory)
+            uint8_t *my_i = oidx + t * k;
+            uint16_t *my_v = oval + t * k;
+            int pos = 0;
+#pragma unroll
+            for (int w = 0; w < NM; ++w) {
+                uint32_t m = active ? gm[w] : 0u;
+                while (m != 0u) {
+                    const int f = 32 * w + (__ffs(m) - 1);
+                    m &= m - 1u;
+                    my_i[pos] = (uint8_t)f;
+                    my_v[pos] = (uint16_t)lds_u16(val_addr(f));
+                    ++pos;
+                }
+            }
+            __syncthreads();  // staging complete
+            // coalesced copy-out of the block's contiguous [nrows][k] index and value blocks
+            const int nib = nrows * k;
+            uint8_t *gi = sg.idx + row0 * k;
+            uint16_t *gv = sg.val + row0 * k;
+            if ((k & 15) == 0) {
+                for (int v = t; v < nib / 16; v += TK_ROWS)
+                    reinterpret_cast<uint4 *>(gi)[v] = reinterpret_cast<const uint4 *>(oidx)[v];
+            } else {
+                for (int v = t; v < nib; v += TK_ROWS) gi[v] = oidx[v];
+            }
+            if ((k & 7) == 0) {
+                for (int v = t; v < nib / 8; v += TK_ROWS)
+                    reinterpret_cast<uint4 *>(gv)[v] = reinterpret_cast<const uint4 *>(oval)[v];
+            } else {
+                for (int v = t; v < nib; v += TK_ROWS) gv[v] = oval[v];
+            }
+            // the next iteration's __syncthreads orders these staging reads before the next writes
+        }
     }
 }
 
@@ -221,13 +320,31 @@ bool rows_kernel_ok(const void *x, int64_t ld, const void *idx, const void *val)
     return (ld * 2) % 16 == 0 && ((uintptr_t)x & 15u) == 0 && ((uintptr_t)idx & 15u) == 0 && ((uintptr_t)val & 15u) == 0;
 }
 
-cudaError_t launch_rows(const TkSegs &sg, int64_t blocks, int d, int k, uint32_t *status_word, cudaStream_t stream) {
-    if (blocks > 0x7FFFFFFF) return cudaErrorInvalidValue;
-    const size_t smem = (size_t)TK_ROWS * d * 2 + ((TK_ROWS * k + 15) & ~15) + (size_t)TK_ROWS * k * 2;
-    auto kern = d == 64 ? topk_rows_bf16_kernel<64> : topk_rows_bf16_kernel<128>;
+template <int D, int KC>
+cudaError_t launch_rows_t(const TkSegs &sg, int k, uint32_t *status_word, cudaStream_t stream) {
+    const size_t smem = (size_t)2 * TK_ROWS * D * 2 + (KC > 0 ? 0 : ((TK_ROWS * k + 15) & ~15) + (size_t)TK_ROWS * k * 2);
+    auto kern = topk_rows_bf16_kernel<D, KC>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    kern<<<(unsigned)blocks, TK_ROWS, smem, stream>>>(sg, k, status_word);
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TK_ROWS, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    const int64_t grid = sg.nb < (int64_t)sms * per_sm ? sg.nb : (int64_t)sms * per_sm;
+    kern<<<(unsigned)grid, TK_ROWS, smem, stream>>>(sg, k, status_word);
     return cudaGetLastError();
+}
+
+cudaError_t launch_rows(TkSegs sg, int64_t blocks, int d, int k, uint32_t *status_word, cudaStream_t stream) {
+    if (blocks > 0x7FFFFFFF) return cudaErrorInvalidValue;
+    sg.nb = blocks;
+    if (d == 64)
+        return k == 8 ? launch_rows_t<64, 8>(sg, k, status_word, stream)
+             : k == 16 ? launch_rows_t<64, 16>(sg, k, status_word, stream)
+                       : launch_rows_t<64, 0>(sg, k, status_word, stream);
+    return k == 8 ? launch_rows_t<128, 8>(sg, k, status_word, stream)
+         : k == 16 ? launch_rows_t<128, 16>(sg, k, status_word, stream)
+                   : launch_rows_t<128, 0>(sg, k, status_word, stream);
 }
 
 // host launcher (called from api.cu after validation)

@@ -27,7 +27,9 @@ __device__ __forceinline__ int count_ge(const uint32_t (&ab)[NW], uint32_t T) {
     asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(s01) : "r"(acc[0]), "r"(acc[1]));
     asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(s23) : "r"(acc[2]), "r"(acc[3]));
     asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(s) : "r"(s01), "r"(s23));  // <= 64 per half: exact
-    return (int)(__uint_as_float(s << 16) + __uint_as_float(s & 0xFFFF0000u));
+    // the two exact integer halves summed, then converted on the FMA pipe (1.5 * 2^23 shifter) rather
+    // than by an F2I on the XU pipe
+    return __float_as_int(__uint_as_float(s << 16) + __uint_as_float(s & 0xFFFF0000u) + 12582912.f) - 0x4B400000;
 }
 
 // max key of the row (>= 0x7F80: a non-finite entry, A14)
@@ -94,6 +96,104 @@ __device__ __forceinline__ void select_masks(const uint32_t (&ab)[NW], int k, ui
             --need;
         }
 #endif
+}
+
+// ---------------------------------------------------------------------------------------------
+// Split row layout (the stand-alone kernel, topk.cu): word i = |x_i| | |x_{i+D/2}| << 16, i < D/2 = NW.
+// The selection is the same function of the row as select_masks (the same T, the same lowest-index
+// tie rule); only the register layout differs, so that the selection masks can be built with one
+// compare and one LOP3 per word (a 0xFFFF-per-half compare result ANDed into bit j of both halves)
+// and land in feature order with four byte permutes, no bit interleaving.
+
+// gm[w] bit b = feature 32w + b has key >= T
+template <int NW>
+__device__ __forceinline__ void ge_masks_split(const uint32_t (&ab)[NW], uint32_t T, uint32_t (&gm)[NW / 16]) {
+    constexpr int NG = NW / 16;  // groups of 16 words: lo halves = features [16g, 16g+16), hi = + NW
+    const uint32_t t2 = T * 0x10001u;
+    uint32_t W[NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+        W[g] = 0u;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            uint32_t m;  // 0xFFFF per half with key >= T
+            asm("set.ge.u32.bf16x2 %0, %1, %2;" : "=r"(m) : "r"(ab[16 * g + j]), "r"(t2));
+            W[g] |= m & (0x10001u << j);
+        }
+    }
+#pragma unroll
+    for (int w = 0; w < NG / 2; ++w) {
+        gm[w] = __byte_perm(W[2 * w], W[2 * w + 1], 0x5410);           // features [32w, 32w+32)
+        gm[w + NG / 2] = __byte_perm(W[2 * w], W[2 * w + 1], 0x7632);  // features NW + [32w, 32w+32)
+    }
+}
+
+// T = the largest threshold with #{key >= T} >= k, cnt = #{key >= T}: the exponent first, walking down
+// from the row max's, then the 7 mantissa bits by bisection, stopping once every lane of the warp has
+// cnt == k (the set {key >= T} is then final: raising T further cannot change it).  (A byte-domain
+// bisection counting with vabsdiff4, two instructions per four keys, measured slower: the count is
+// bound by the ALU pipe, which vabsdiff4 shares with the compare it replaces; profiles/r02_topk.md.)
+// Call with the whole warp converged.
+template <int NW>
+__device__ __forceinline__ uint32_t threshold_split(const uint32_t (&ab)[NW], int k, uint32_t mx, int &cnt) {
+    int e = (int)((mx > 0x7FFFu ? 0x7FFFu : mx) >> 7);
+#pragma unroll 1
+    for (;;) {  // count_ge(0) = 2 NW >= k ends the walk at e = 0 at the latest
+        cnt = count_ge(ab, (uint32_t)e << 7);
+        if (cnt >= k || e == 0) break;
+        --e;
+    }
+    uint32_t T = (uint32_t)e << 7;
+#pragma unroll 1
+    for (int bit = 6; bit >= 0; --bit) {
+        if (__all_sync(0xffffffffu, cnt == k)) break;
+        const uint32_t cand = T | (1u << bit);
+        const int c = count_ge(ab, cand);
+        if (c >= k) {
+            T = cand;
+            cnt = c;
+        }
+    }
+    return T;
+}
+
+// Exact selection masks (every key > T, then the lowest-index keys == T, A2).
+template <int NW>
+__device__ __forceinline__ void select_masks_split(const uint32_t (&ab)[NW], int k, uint32_t (&gm)[NW / 16], uint32_t mx) {
+    constexpr int NM = NW / 16;
+    int cnt;
+    const uint32_t T = threshold_split(ab, k, mx, cnt);
+    ge_masks_split(ab, T, gm);
+    if (cnt != k) {  // ties at T: keep key > T, add the lowest-index keys == T
+        uint32_t em[NM];
+        ge_masks_split(ab, T + 1u, em);  // T + 1 <= 0x7F80 (+inf) on finite rows
+        int need = k;
+#pragma unroll
+        for (int w = 0; w < NM; ++w) {
+            const uint32_t gt = em[w];
+            em[w] = gm[w] & ~gt;  // key == T
+            gm[w] = gt;
+            need -= __popc(gt);
+        }
+#ifndef SFA_FAULT_TOPK_TIE_HIGH
+#pragma unroll
+        for (int w = 0; w < NM; ++w)
+            while (need > 0 && em[w] != 0u) {  // lowest-index ties first (A2)
+                gm[w] |= em[w] & (0u - em[w]);
+                em[w] &= em[w] - 1u;
+                --need;
+            }
+#else  // negative control (tools/gpu_mutants.sh): ties taken from the highest index
+#pragma unroll
+        for (int w = NM - 1; w >= 0; --w)
+            while (need > 0 && em[w] != 0u) {
+                const uint32_t hb = 0x80000000u >> __clz(em[w]);
+                gm[w] |= hb;
+                em[w] &= ~hb;
+                --need;
+            }
+#endif
+    }
 }
 
 }  // namespace tk

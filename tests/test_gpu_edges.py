@@ -41,6 +41,7 @@ def run_case(lib, seed, B, H, H_kv, n, d, d_v, k, dtype, kernel, causal=True, n_
     (1, 4, 2, 300, 128, 128, 4),     # GQA, ragged n, k = 4: most pairs are non-edges (12 % overlap)
     (1, 2, 1, 385, 128, 128, 16),    # 3 tiles + 1
     (2, 2, 2, 257, 64, 128, 8),      # d = 64
+    (2, 3, 3, 300, 64, 64, 8),       # GPT-2 head shape: d = d_v = 64 (OT over the zero-padded V copy)
     (1, 2, 2, 1, 128, 128, 2),       # single token
     (1, 2, 1, 200, 128, 128, 1),     # k = 1: edge iff the same single feature (many empty rows)
 ])

@@ -114,14 +114,15 @@ def test_variant_score_tile_is_exact_overlap_sum(lib, variant, d, k):
     (2, 2, 2, 300, 64, 128, 8),     # MHA, d = 64, ragged
     (1, 2, 1, 515, 128, 128, 32),
     (1, 2, 2, 1, 128, 128, 4),      # a single token
-    (1, 2, 2, 700, 64, 64, 8),      # d_v = 64 (pp)
+    (1, 2, 2, 700, 64, 64, 8),      # d_v = 64 (pp; ot over the zero-padded V copy)
+    (1, 4, 2, 333, 128, 64, 16),    # d_v = 64, d = 128, GQA, ragged
 ])
 @pytest.mark.parametrize("causal", [True, False])
 def test_variant_against_oracle(lib, variant, shape, causal):
     import torch
     B, H, H_kv, n, d, d_v, k = shape
-    if variant in ("ot", "oth") and d_v != 128:
-        pytest.skip("ot / oth kernels need d_v = 128 (M of the transposed product)")
+    if variant == "oth" and d_v != 128:
+        pytest.skip("the oth kernel needs d_v = 128 (M of the transposed product)")
     q, kx, v = host_qkv(56, B, H, H_kv, n, d, d_v, "bf16")
     qi, qv = oracle_codes(q, k)
     ki, kv = oracle_codes(kx, k)
@@ -144,4 +145,20 @@ def test_variant_peaked_rows_and_q_pos0(lib, variant):
                           to_torch(kv, "bf16"), to_torch(v, "bf16"), d=d, scale=0.5, q_pos0=200,
                           kernel=_kern(lib, variant))
     torch.cuda.synchronize()
+    assert_attn_close(from_torch(o), from_torch(lse), o_ref, l_ref, "bf16")
+
+
+def test_ot_gpt2_config_dv64(lib):
+    """BASELINE configs[1] (B=8, H=12, n=1024, d=64, d_v=64, k=8, causal) on SM100_OT: d_v = 64 runs the
+    d_v = 128 transposed P.V over V's zero-padded fp16 copy; every element against the oracle."""
+    import torch
+    B, H, H_kv, n, d, d_v, k = 8, 12, 12, 1024, 64, 64, 8
+    q, kx, v = host_qkv(11, B, H, H_kv, n, d, d_v, "bf16")
+    qi, qv = oracle_codes(q, k)
+    ki, kv = oracle_codes(kx, k)
+    o_ref, l_ref = oracle.attn_fwd(qi, qv, ki, kv, v, d=d, causal=True)
+    o, lse = lib.attn_fwd(to_torch(qi, "u8"), to_torch(qv, "bf16"), to_torch(ki, "u8"), to_torch(kv, "bf16"),
+                          to_torch(v, "bf16"), d=d, causal=True, kernel=lib.KERNEL_SM100_OT)
+    torch.cuda.synchronize()
+    assert o.shape[-1] == 64
     assert_attn_close(from_torch(o), from_torch(lse), o_ref, l_ref, "bf16")

@@ -32,6 +32,7 @@ def test_parity(lib, kernel, window):
 @pytest.mark.parametrize("kernel", [OT, SIMT])
 def test_shapes(lib, kernel):
     run_case(lib, 72, 2, 2, 2, 257, 64, 128, 8, "bf16", kernel, 100)            # d = 64, MHA pairing
+    run_case(lib, 77, 2, 3, 3, 300, 64, 64, 8, "bf16", kernel, 90)              # d = d_v = 64 (GPT-2 heads)
     run_case(lib, 73, 1, 2, 1, 200, 128, 128, 16, "bf16", kernel, 64, n_kv=700, q_pos0=500)  # chunk at q_pos0
     run_case(lib, 74, 1, 2, 1, 400, 128, 128, 4, "bf16", kernel, 150, edges_only=True)       # + R2
 
