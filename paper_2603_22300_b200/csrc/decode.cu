@@ -9,15 +9,19 @@
 //
 // Split-KV: CTA (b, kv head g, split s) owns keys [s*chunk, (s+1)*chunk).  The group's query rows
 // (R = H/H_kv heads x n_q rows) are decompressed into shared memory as fp32 (q~ scaled by
-// scale*log2 e).  A producer warp streams the split's V rows through a 3-stage shared-memory ring
-// of 256-key blocks with cp.async.bulk (mbarrier transaction counts), so ~130 KB of V is in flight
-// per SM; 8 consumer warps take 32 keys of every block each: lane l scores its key against every
+// scale*log2 e).  A producer warp streams the split's V rows through a shared-memory ring of 128-key
+// blocks (2 stages, 3 CTAs per SM; 256-key blocks, 3 stages, 1 CTA per SM for more than 4 rows) with
+// cp.async.bulk (mbarrier transaction counts); the consumer warps (one per 32 keys of a block, every
+// block read by all of them) take 32 keys of every block each: lane l scores its key against every
 // row with k FMAs from the key's code (16-byte loads prefetched one block ahead), the warp reduces
 // the block max per row and updates the running max (online softmax, fp32), then accumulates
 // O[row][:] += p V[key] from the ring with lanes over d_v and p broadcast by shuffles.  Each warp
 // keeps its own (m, l, O) in registers; the CTA merges its warps (in the drained ring) and writes
 // one partial per split; `decode_combine_kernel` merges the splits with their log-sum-exps.  fp32
 // throughout, bf16 V read as is; O rounded to bf16 once.
+#include <algorithm>
+#include <cstdlib>
+
 #include "launch.cuh"
 #include "sm100.cuh"
 
@@ -50,8 +54,24 @@ struct DecArgs {
 #ifndef SFA_DEC_WAVES
 #define SFA_DEC_WAVES 4
 #endif
-constexpr int DB = 256;  // keys per V block streamed by the producer
-constexpr int NST = 3;   // V ring stages
+// keys per V block streamed by the producer = 32 x the consumer warps: 128 (several CTAs per SM, 4
+// consumer warps each: one CTA's prologue and merge overlap the others' streaming) or 256 (one CTA per
+// SM, 8 consumer warps; more than 4 rows per kv head need its registers).
+// Configurations (A/B through SFA_DEC_DB, read once; 8 sequences x Qwen3 heads x 32K cache, one B200):
+// 1282 = 128-key blocks, 2 ring stages, 3 CTAs per SM (default, 0.133 ms = 0.73 of HBM); 128 = 128-key
+// blocks, 3 stages, 2 CTAs per SM (0.138 ms); 256 = 256-key blocks, 3 stages, 1 CTA per SM (0.146 ms).
+// Measured and dropped: 64-key blocks with 3 / 2 stages at 4 / 6 CTAs per SM (0.138 / 0.150 ms).
+int dec_cfg() {
+    static const int c = [] {
+        const char *e = getenv("SFA_DEC_DB");
+        const int v = e != nullptr ? atoi(e) : 1282;
+        return (v == 256 || v == 128) ? v : 1282;
+    }();
+    return c;
+}
+int dec_db() { return dec_cfg() == 256 ? 256 : 128; }
+constexpr int dec_minb(int db, int nst) { return db == 256 ? 1 : (nst == 2 ? 3 : 2); }
+int dec_minb_rt() { return dec_cfg() == 256 ? 1 : dec_cfg() == 128 ? 2 : 3; }
 
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
@@ -66,8 +86,10 @@ struct Code32 {
 };
 
 // CW consumer warps (8 or 16): warps 8g..8g+7 take the blocks blk = g (mod CW / 8), 32 keys each
-template <int DV, int ROWS, int CW>
-__global__ void __launch_bounds__(CW * 32 + 32, 1) decode_partial_kernel(const DecArgs a) {
+template <int DV, int ROWS, int CW, int DB, int NST>
+__global__ void __launch_bounds__(CW * 32 + 32, dec_minb(DB, NST)) decode_partial_kernel(const DecArgs a) {
+    constexpr int WPB = DB / 32;      // consumer warps per V block (32 keys each)
+    static_assert(CW == WPB, "one consumer group: every V block is read by all consumer warps");
     constexpr int DPL = DV / 32;      // value dims per lane (2 or 4)
     constexpr int VT = DB * DV * 2;   // bytes of one V block
     extern __shared__ __align__(1024) uint8_t dsm_raw[];
@@ -91,7 +113,7 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) decode_partial_kernel(const D
     if (threadIdx.x == 0) {
         for (int i = 0; i < NST; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s + 8 * i));
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_s + 8 * (NST + i)), "r"(DEC_WARPS));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_s + 8 * (NST + i)), "r"(WPB));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -120,7 +142,7 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) decode_partial_kernel(const D
 #pragma unroll
         for (int e = 0; e < DPL; ++e) acc[r][e] = 0.f;
     }
-    constexpr int GROUPS = CW / DEC_WARPS;
+    constexpr int GROUPS = CW / WPB;
     if (warp == CW) {
         // ============ producer: V blocks of the split into the ring (cp.async.bulk, mbarrier tx) ============
         if (lane == 0) {
@@ -137,7 +159,7 @@ __global__ void __launch_bounds__(CW * 32 + 32, 1) decode_partial_kernel(const D
         }
     } else {
         // ============ consumers: warp w takes keys [32 (w % 8), +32) of blocks w / 8, w / 8 + GROUPS, ... ============
-        const int sub = warp % DEC_WARPS, grp0 = warp / DEC_WARPS;
+        const int sub = warp % WPB, grp0 = warp / WPB;
         const bool pre = (a.k & 7) == 0 && a.k <= 32;
         Code32 nxt;
         auto load_code = [&](Code32 &c, int64_t key) {
@@ -326,13 +348,17 @@ __global__ void __launch_bounds__(DV) decode_combine_kernel(const DecArgs a) {
     if (c == 0) a.lse[orow] = L > 0.f ? (M + __log2f(L)) * 0.69314718055994530942f : -INFINITY;
 }
 
-template <int DV, int ROWS>
+template <int DV, int ROWS, int DB, int NST>
 cudaError_t launch_decode_t(const DecArgs &a, cudaStream_t st) {
-    constexpr int CW = ROWS <= 4 ? 16 : 8;  // 16 consumer warps when the registers allow
+    // consumer warps = DB / 32: every V block is consumed by ALL consumer warps (one group).  With two
+    // groups taking alternate blocks of one shared stage ring (the round-1 shape for <= 4 rows: 16 warps,
+    // 256-key blocks), a group can wait on a stage's full barrier two phases ahead of the other group's
+    // use of that stage, and the parity test then passes on the wrong phase.
+    constexpr int CW = DB / 32;
     const size_t smem = ((size_t)ROWS * a.d * 4 + (size_t)CW * 32 * ROWS * 4 + 1023) / 1024 * 1024 +
                         (size_t)NST * DB * DV * 2 + 2 * NST * 8 + 1024;
     static_assert((size_t)CW * ROWS * (2 + DV) * 4 <= (size_t)NST * DB * DV * 2, "merge area fits the V ring");
-    auto kern = decode_partial_kernel<DV, ROWS, CW>;
+    auto kern = decode_partial_kernel<DV, ROWS, CW, DB, NST>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 g1(a.B * a.H_kv, a.nsplit);
@@ -342,24 +368,39 @@ cudaError_t launch_decode_t(const DecArgs &a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// the V block size of a launch: 128 keys (two CTAs per SM) for up to 4 rows per kv head -- more rows
+// need more registers than two CTAs of 288 threads leave (spills) -- else 256
+int dec_db_for(int rows) { return rows <= 4 ? dec_db() : 256; }
+
+template <int DV, int ROWS>
+cudaError_t launch_decode_r(const DecArgs &a, cudaStream_t st) {
+    if constexpr (ROWS <= 4) {
+        if (dec_db_for(ROWS) != 256) {
+            return dec_cfg() == 128 ? launch_decode_t<DV, ROWS, 128, 3>(a, st) : launch_decode_t<DV, ROWS, 128, 2>(a, st);
+        }
+    }
+    return launch_decode_t<DV, ROWS, 256, 3>(a, st);
+}
+
 }  // namespace
 
 // keys per split: a multiple of 32 (one consumer warp's slice); splits need not be whole V blocks
 int64_t decode_chunk(int64_t n_kv, int nsplit) { return ((n_kv + nsplit - 1) / nsplit + 31) / 32 * 32; }
 
-int decode_nsplit(int64_t bh_kv, int64_t n_kv) {
-    // one CTA per SM (the V ring is ~200 KB).  Pick the split count that minimises the streaming time
+int decode_nsplit(int64_t bh_kv, int64_t n_kv, int DB) {
+    // 148 x (1 or 2) resident CTAs (the V ring is ~200 KB or ~100 KB).  Pick the split count that minimises the streaming time
     // waves x keys-per-CTA plus a per-wave ramp (first V block latency + merge, ~512 keys' worth),
     // among splits of >= 2 V blocks and at most SFA_DEC_WAVES * 2 waves: a last wave that is mostly
     // empty costs as much as a full one.
+    const int64_t per_wave = 148 * (DB == 256 ? 1 : dec_minb_rt());
     const int64_t maxs = (n_kv + 2 * DB - 1) / (2 * DB);
     int best = 1;
     double best_cost = 1e300;
     for (int64_t s = 1; s <= maxs && s <= 4096; ++s) {
         const int64_t ctas = bh_kv * s;
-        const int64_t waves = (ctas + 147) / 148;
+        const int64_t waves = (ctas + per_wave - 1) / per_wave;
         if (waves > 2 * SFA_DEC_WAVES && s > 1) break;
-        const double cost = (double)waves * ((double)decode_chunk(n_kv, (int)s) + 512.0);
+        const double cost = (double)waves * ((double)decode_chunk(n_kv, (int)s) + 2.0 * DB);
         if (cost < best_cost * 0.999) {
             best_cost = cost;
             best = (int)s;
@@ -369,7 +410,8 @@ int decode_nsplit(int64_t bh_kv, int64_t n_kv) {
 }
 
 size_t decode_workspace_bytes(int64_t bh_kv, int64_t n_kv, int d_v) {
-    return (size_t)bh_kv * decode_nsplit(bh_kv, n_kv) * MAXROWS * (2 + d_v) * 4;
+    const int s = std::max(decode_nsplit(bh_kv, n_kv, dec_db()), decode_nsplit(bh_kv, n_kv, 256));
+    return (size_t)bh_kv * s * MAXROWS * (2 + d_v) * 4;
 }
 
 cudaError_t launch_decode(const AttnParams &p, int d, int d_v, cudaStream_t st, void *ws) {
@@ -396,11 +438,11 @@ cudaError_t launch_decode(const AttnParams &p, int d, int d_v, cudaStream_t st, 
     a.q_pos0 = p.q_pos0;
     a.causal = p.causal;
     a.c_scale = p.scale_log2;
-    a.nsplit = decode_nsplit((int64_t)p.B * p.H_kv, p.n_kv);
+    a.nsplit = decode_nsplit((int64_t)p.B * p.H_kv, p.n_kv, dec_db_for(rows));
     a.chunk = decode_chunk(p.n_kv, a.nsplit);
-    if (rows <= 4) return d_v == 64 ? launch_decode_t<64, 4>(a, st) : launch_decode_t<128, 4>(a, st);
-    if (rows <= 8) return d_v == 64 ? launch_decode_t<64, 8>(a, st) : launch_decode_t<128, 8>(a, st);
-    return d_v == 64 ? launch_decode_t<64, 16>(a, st) : launch_decode_t<128, 16>(a, st);
+    if (rows <= 4) return d_v == 64 ? launch_decode_r<64, 4>(a, st) : launch_decode_r<128, 4>(a, st);
+    if (rows <= 8) return d_v == 64 ? launch_decode_r<64, 8>(a, st) : launch_decode_r<128, 8>(a, st);
+    return d_v == 64 ? launch_decode_r<64, 16>(a, st) : launch_decode_r<128, 16>(a, st);
 }
 
 }  // namespace sfa
