@@ -132,7 +132,8 @@ __device__ __forceinline__ void ge_masks_split(const uint32_t (&ab)[NW], uint32_
 // from the row max's, then the 7 mantissa bits by bisection, stopping once every lane of the warp has
 // cnt == k (the set {key >= T} is then final: raising T further cannot change it).  (A byte-domain
 // bisection counting with vabsdiff4, two instructions per four keys, measured slower: the count is
-// bound by the ALU pipe, which vabsdiff4 shares with the compare it replaces; profiles/r02_topk.md.)
+// bound by the ALU pipe, which vabsdiff4 shares with the compare it replaces; so did moving 3/8 of the
+// compares to the FMA pipe as fma.sat.f16x2 on the keys read as f16 -- profiles/r02_topk.md.)
 // Call with the whole warp converged.
 template <int NW>
 __device__ __forceinline__ uint32_t threshold_split(const uint32_t (&ab)[NW], int k, uint32_t mx, int &cnt) {
