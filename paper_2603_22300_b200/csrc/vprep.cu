@@ -53,15 +53,7 @@ __global__ void __launch_bounds__(256) v_to_f16_kernel(const uint4 *__restrict__
 #endif
     const uint4 *src = v + (int64_t)bh * vec_per_head;
     uint4 *dst = reinterpret_cast<uint4 *>(out) + (int64_t)bh * out_per_head;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < out_per_head;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = cin == cout ? 0 : i / cout;
-        const int c = cin == cout ? 0 : (int)(i - row * cout);
-        if (c >= cin) {
-            dst[i] = make_uint4(0u, 0u, 0u, 0u);
-            continue;
-        }
-        const uint4 x = __ldcs(src + (cin == cout ? i : row * cin + c));
+    const auto cvt = [sc](const uint4 x) {
         const uint32_t w[4] = {x.x, x.y, x.z, x.w};
         uint32_t o[4];
 #pragma unroll
@@ -69,7 +61,19 @@ __global__ void __launch_bounds__(256) v_to_f16_kernel(const uint4 *__restrict__
             const __half2 h = __floats2half2_rn(__uint_as_float(w[q] << 16) * sc, __uint_as_float(w[q] & 0xFFFF0000u) * sc);
             o[q] = *reinterpret_cast<const uint32_t *>(&h);
         }
-        dst[i] = make_uint4(o[0], o[1], o[2], o[3]);
+        return make_uint4(o[0], o[1], o[2], o[3]);
+    };
+    if (cin == cout) {  // unpadded copy: a plain streaming loop
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < out_per_head;
+             i += (int64_t)gridDim.x * blockDim.x)
+            dst[i] = cvt(__ldcs(src + i));
+    } else {
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < out_per_head;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t row = i / cout;
+            const int c = (int)(i - row * cout);
+            dst[i] = c < cin ? cvt(__ldcs(src + row * cin + c)) : make_uint4(0u, 0u, 0u, 0u);
+        }
     }
     }
 }
