@@ -8,7 +8,7 @@ B() { python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 
 SEL_ATTN="tests/test_gpu_attn.py tests/test_gpu_sm100.py tests/test_gpu_window.py"
 run() {  # $1 = fault macro (or none), $2 = tests
   if [ "$1" = none ]; then SFA_NVCC_FLAGS="" B; else SFA_NVCC_FLAGS="-D$1" B; fi
-  timeout 400 python -m pytest $2 -q -m "gpu and not slow" -k "not pp and not pair and not wide" -p no:cacheprovider > gpurun_out/mut_$1.log 2>&1
+  timeout -k 10 400 python -m pytest $2 -q -m "gpu and not slow" -k "not pp and not pair and not wide" -p no:cacheprovider > gpurun_out/mut_$1.log 2>&1
   res=$(tail -1 gpurun_out/mut_$1.log)
   echo "$1 | $2 | $res" | tee -a $out
 }
