@@ -10,10 +10,11 @@ from paper_2603_22300_b200 import inputs, sfa  # noqa: E402
 
 L = sfa.lib()
 P = lambda t: ctypes.c_void_p(t.data_ptr())
-H, n, d, k = 12, 1024, 64, 8
+H, d, k = 12, 64, 8
+shapes = [(B, 1024) for B in (1, 2, 4, 8, 16, 32)] + [(8, 2048), (2, 4096), (1, 8192), (1, 16384)]
 for kern_name in sys.argv[1:] or ["sm100", "ot"]:
     kern = {"sm100": sfa.KERNEL_SM100, "ot": sfa.KERNEL_SM100_OT}[kern_name]
-    for B in (1, 2, 4, 8, 16, 32):
+    for B, n in shapes:
         q = sfa.gen_fill(torch.empty((B, H, n, d), dtype=torch.bfloat16, device="cuda"), 11, inputs.TID_Q)
         kx = sfa.gen_fill(torch.empty((B, H, n, d), dtype=torch.bfloat16, device="cuda"), 11, inputs.TID_K)
         v = sfa.gen_fill(torch.empty((B, H, n, d), dtype=torch.bfloat16, device="cuda"), 11, inputs.TID_V)
@@ -38,5 +39,5 @@ for kern_name in sys.argv[1:] or ["sm100", "ot"]:
                 ts.append(e0.elapsed_time(e1) * 1e3)
         ts.sort()
         tiles = B * H * sum(2 * p + 2 for p in range(n // 256))  # 2-tile items (h, 2p, 2p+1): 2p+2 key tiles
-        print(f"{kern_name} B={B:3d} attention {ts[len(ts) // 2]:8.1f} us  item-tile-steps {tiles:6d}  "
+        print(f"{kern_name} B={B:3d} n={n:6d} attention {ts[len(ts) // 2]:8.1f} us  item-tile-steps {tiles:6d}  "
               f"per SM {tiles / 148:7.1f}  us/step/SM {ts[len(ts) // 2] / (tiles / 148):6.2f}", flush=True)
