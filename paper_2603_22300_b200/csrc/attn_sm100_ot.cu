@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                 }
             }
             mbar_wait(BAR(SFULL + t), sc & 1);
-            if (lane == 0 && wq == 0) TLREC(0x1000 | (t << 10) | (j & 1023));
+            if (lane == 0 && wq == 0) TLREC(0x1000 | (t << 10) | (sc & 511));
             tc_fence_after();
             uint32_t s[4][32];
             float mq[4];  // four independent max chains; keys 64-127 load while 0-63 are reduced
@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                 }
             }
             const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * cs;
-            if (lane == 0 && wq == 0) TLREC(0x5000 | (t << 10) | (j & 1023));
+            if (lane == 0 && wq == 0) TLREC(0x5000 | (t << 10) | (sc & 511));
             const float m_new = fmaxf(m, mx);
             // O^T columns are shared by the whole warpgroup: rescale all of tile t or none of it
             const bool rescale = named_bar_or(bar_id, 128, m_new > m + 8.f);
@@ -533,7 +533,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
 #else
             const bool rescale_o = rescale;
 #endif
-            if (lane == 0 && wq == 0) TLREC(0x6000 | (t << 10) | (j & 1023));
+            if (lane == 0 && wq == 0) TLREC(0x6000 | (t << 10) | (sc & 511));
             if (rescale) {
                 const float alpha = (m_new == -INFINITY) ? 1.f : fast_exp2(m - m_new);
                 l *= alpha;
@@ -563,10 +563,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                     }
                 }
                 if (h == 0) {
-                    if (lane == 0 && wq == 0) TLREC(0x4000 | (t << 10) | (j & 1023));
+                    if (lane == 0 && wq == 0) TLREC(0x4000 | (t << 10) | (sc & 511));
                     // the P buffer is free (the previous P.V, over all items, has read it)
                     mbar_wait(BAR(PEMPTY), (sc & 1) ^ 1);
-                    if (lane == 0 && wq == 0) TLREC(0x7000 | (t << 10) | (j & 1023));
+                    if (lane == 0 && wq == 0) TLREC(0x7000 | (t << 10) | (sc & 511));
                     if (rescale_o && j > 0) {
                         named_bar_sync(bar_id, 128);  // every row's alpha is in f_t
                         tc_fence_after();
@@ -599,11 +599,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(BAR(PFULL));
-            if (lane == 0 && wq == 0) TLREC(0x2000 | (t << 10) | (j & 1023));
+            if (lane == 0 && wq == 0) TLREC(0x2000 | (t << 10) | (sc & 511));
             ++sc;
         }
         // ---- epilogue (step 8): O = 2^e (sum_j P'_j V'_j) / l, V' = V 2^-e (vprep.cu)
         mbar_wait(BAR(OFULL), m_ & 1);
+        if (lane == 0 && wq == 0) TLREC(0x8000 | (t << 10) | ((2 * m_) & 511));
         tc_fence_after();
         const float inv = l > 0.f ? __uint_as_float((uint32_t)(127 + vprep_head_exp(__ldg(p.v_amax + b * p.H_kv + g))) << 23) / l : 0.f;
         f_t[r] = inv;
@@ -641,6 +642,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
             }
             p.lse[orow] = l > 0.f ? (m + __log2f(l) - P_SHIFT) * 0.69314718055994530942f : -INFINITY;
         }
+        if (lane == 0 && wq == 0) TLREC(0x8000 | (t << 10) | ((2 * m_ + 1) & 511));
         // both tiles' staging (the dead P buffer, where the other tile's rows interleave) is read before
         // either tile stores the next item's P
         named_bar_sync(5, 2 * BM);
@@ -726,7 +728,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
                             }
                             mbar_wait(BAR(VFULL), vc & 1);  // one V stage
                             mbar_wait(BAR(PFULL), vc & 1);  // one P per key tile
-                            TLREC(0x3000 | (j & 1023));
+                            TLREC(0x3000 | (vc & 511));
                             if (j == 0 && m > 0) mbar_wait(BAR(OEMPTY), (m - 1) & 1);  // O^T read out
                             tc_fence_after();
                             mma_O(j > 0, 0, 0);
