@@ -612,17 +612,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) attn_sm100_ot_kernel(const __grid
         // O^T lane r = feature r: scale column c by 1/l of query c, transpose through shared memory
         // (the dead P buffer; row = query, 16-byte chunk swizzled by row) for row-contiguous stores
         const uint32_t so = sbase + C::OFF_P + (uint32_t)t * (BM * DV * 2);
+        // per element: one FMUL, one cvt, one LOP3 (the chunk swizzle; (qq & 15) = (c & 15) is a constant of
+        // the unrolled loop) and one STS with the row offset as an immediate; 1/l four queries per LDS.128;
+        // the TMEM loads two 32-column blocks at a time (one wait per pair)
+        const uint32_t rbase = so + (uint32_t)(r & 7) * 2, rh = (uint32_t)(r >> 3) << 4;
 #pragma unroll 1
-        for (int q = 0; q < BM / 32; ++q) {
-            uint32_t o[32];
-            tmem_ld32(tO + 32 * q, o);
+        for (int q = 0; q < BM / 32; q += 2) {
+            uint32_t o[2][32];
+            tmem_ld32(tO + 32 * q, o[0]);
+            tmem_ld32(tO + 32 * q + 32, o[1]);
             tmem_ld_wait();
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                const int qq = 32 * q + c;
-                const float v = __uint_as_float(o[c]) * f_t[qq];
-                const uint32_t addr = so + (uint32_t)qq * (DV * 2) + ((uint32_t)((r >> 3) ^ (qq & 15)) << 4) + (uint32_t)(r & 7) * 2;
-                sts_u16(addr, __bfloat16_as_ushort(__float2bfloat16_rn(v)));
+            for (int hq = 0; hq < 2; ++hq) {
+                const uint32_t qb = rbase + (uint32_t)(32 * (q + hq)) * (DV * 2);
+#pragma unroll
+                for (int c4 = 0; c4 < 32; c4 += 4) {
+                    const float4 iv = *reinterpret_cast<const float4 *>(f_t + 32 * (q + hq) + c4);
+                    const float ivs[4] = {iv.x, iv.y, iv.z, iv.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int c = c4 + u;
+                        const float v = __uint_as_float(o[hq][c]) * ivs[u];
+                        sts_u16(qb + (uint32_t)c * (DV * 2) + (rh ^ ((uint32_t)(c & 15) << 4)),
+                                __bfloat16_as_ushort(__float2bfloat16_rn(v)));
+                    }
+                }
             }
         }
         // O^T is read out: the next item's first P.V may overwrite it
