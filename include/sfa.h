@@ -172,8 +172,8 @@ SFA_API sfa_status sfa_attn_fwd_prepared(const sfa_attn_desc *desc, const uint8_
  *   Key j is allowed for query row i iff j <= q_pos0 + i (if causal) and j / 128 is listed for the
  *   row's query block i / 128; rows without an allowed key get O = 0, LSE = -inf.  Runs steps 3-8 on
  *   the default tensor-core kernel (persistent tile scheduler over the listed tiles only).
- *   Supported: bf16, d_v = 128, H / H_kv even, edges_only = 0, window = 0, kernel AUTO or SM100_OT;
- *   else SFA_ERR_UNSUPPORTED.  max_sel >= 1; block_sel 4-byte aligned.  Workspace as sfa_attn_fwd. */
+ *   Supported: bf16, H / H_kv even, edges_only = 0, window = 0, and the desc resolving to SM100_OT
+ *   (kernel AUTO with d_v = 128, or SFA_KERNEL_SM100_OT with d_v = 64 or 128); else SFA_ERR_UNSUPPORTED.  max_sel >= 1; block_sel 4-byte aligned.  Workspace as sfa_attn_fwd. */
 SFA_API sfa_status sfa_attn_fwd_blocksel(const sfa_attn_desc *desc, const uint8_t *q_idx, const void *q_val,
                                          const uint8_t *k_idx, const void *k_val, const void *v,
                                          const int32_t *block_sel, int32_t max_sel, void *o, float *lse,

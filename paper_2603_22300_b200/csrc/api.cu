@@ -347,7 +347,7 @@ sfa_status sfa_attn_fwd_blocksel(const sfa_attn_desc *desc, const uint8_t *q_idx
                                  sfa_stream_t stream) {
     sfa_status s = validate_desc(desc);
     if (s != SFA_OK) return s;
-    if (desc->dtype != SFA_BF16 || desc->d_v != 128 || (desc->H / desc->H_kv) % 2 != 0 || desc->edges_only ||
+    if (desc->dtype != SFA_BF16 || (desc->H / desc->H_kv) % 2 != 0 || desc->edges_only ||
         desc->window > 0 || resolve_kernel(desc) != SFA_KERNEL_SM100_OT)
         return SFA_ERR_UNSUPPORTED;
     if (!q_idx || !q_val || !k_idx || !k_val || !v || !o || !lse || !workspace || !block_sel || max_sel < 1)

@@ -260,7 +260,8 @@ def attn_fwd_blocksel(q_idx, q_val, k_idx, k_val, v, block_sel, *, d, causal=Tru
     if block_sel.dtype != torch.int32 or block_sel.dim() != 4 or not block_sel.is_contiguous() or \
             tuple(block_sel.shape[:3]) != (B, H_kv, (n_q + 127) // 128):
         raise ValueError("block_sel: contiguous int32 [B, H_kv, ceil(n_q/128), max_sel]")
-    desc = _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, KERNEL_AUTO, _dt(v))
+    # block selection runs on SM100_OT (named explicitly: AUTO would pick SM100 for d_v = 64)
+    desc = _desc_from_codes(q_idx, k_idx, v, d, causal, scale, q_pos0, KERNEL_SM100_OT, _dt(v))
     nb = workspace_bytes(desc)
     if workspace is None:
         workspace = torch.empty(max(nb, 16), dtype=torch.uint8, device=v.device)

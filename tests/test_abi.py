@@ -137,6 +137,9 @@ def test_n4_semantics_validation(sfa):
               dict(dtype=sfa.SFA_F32), dict(kernel=sfa.KERNEL_SM100_PP)):
         assert bsf(ctypes.byref(desc(sfa, **b)), *([dv16] * 6), 4, dv16, dv16, dv16, 1 << 30, None) == 3, b
     assert bsf(ctypes.byref(desc(sfa)), *([dv16] * 6), 4, dv16, dv16, dv16, 16, None) == 4             # workspace
+    # d_v = 64 runs when the desc names SM100_OT (AUTO picks SM100 for d_v = 64): it gets to the workspace check
+    d64 = desc(sfa, d_v=64, kernel=sfa.KERNEL_SM100_OT)
+    assert bsf(ctypes.byref(d64), *([dv16] * 6), 4, dv16, dv16, dv16, 16, None) == 4
     # the round-1 ablation kernels PAIR / WIDE were removed in round 2: their numbers stay reserved
     for kern in (sfa.KERNEL_SM100_PAIR, sfa.KERNEL_SM100_WIDE):
         assert L.sfa_attn_fwd(ctypes.byref(desc(sfa, kernel=kern)), *([ctypes.c_void_p(16)] * 8), 1 << 30, None) == 3

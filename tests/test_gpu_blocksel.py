@@ -39,6 +39,7 @@ def make_sel(rng, B, H_kv, n_q, n_kv, max_sel, mode):
     (1, 4, 2, 1000, 128, 128, 16),   # GQA R = 2, ragged
     (2, 8, 2, 700, 64, 128, 8),      # d = 64 keys, R = 4
     (1, 2, 1, 384, 128, 128, 4),
+    (1, 4, 2, 500, 64, 64, 8),       # d = d_v = 64 (OT over the zero-padded V copy)
 ])
 @pytest.mark.parametrize("causal", [True, False])
 def test_blocksel_against_oracle(lib, mode, shape, causal):
@@ -57,7 +58,7 @@ def test_blocksel_against_oracle(lib, mode, shape, causal):
     assert_attn_close(from_torch(o), from_torch(lse), o_ref, l_ref, "bf16")
     if mode == "all":  # every tile listed: the plain forward, bit for bit
         o2, l2 = lib.attn_fwd(to_torch(qi, "u8"), to_torch(qv, "bf16"), to_torch(ki, "u8"), to_torch(kv, "bf16"),
-                              to_torch(v, "bf16"), d=d, causal=causal)
+                              to_torch(v, "bf16"), d=d, causal=causal, kernel=lib.KERNEL_SM100_OT)
         torch.cuda.synchronize()
         assert torch.equal(o, o2) and torch.equal(lse, l2)
 
