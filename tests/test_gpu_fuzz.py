@@ -58,3 +58,28 @@ def test_random_shape(lib, i):
                               edges_only=edges)
         torch.cuda.synchronize()
         assert_attn_close(from_torch(o), from_torch(lse), o_ref, l_ref, "bf16")
+
+
+def draw_bwd(i):
+    rng = np.random.default_rng(5000 + i)
+    B = int(rng.integers(1, 3))
+    H_kv = int(rng.integers(1, 3))
+    R = int(rng.choice([1, 2, 3, 4]))
+    d = int(rng.choice([64, 128]))
+    d_v = int(rng.choice([64, 128]))
+    k = int(rng.integers(1, d + 1)) if rng.random() < 0.3 else int(rng.choice([4, 8, 16]))
+    n_kv = int(rng.integers(1, 500))
+    n = n_kv if rng.random() < 0.6 else int(rng.integers(1, n_kv + 1))
+    q_pos0 = n_kv - n if rng.random() < 0.7 else int(rng.integers(0, n_kv - n + 1))
+    causal = bool(rng.random() < 0.75)
+    return B, R * H_kv, H_kv, n, n_kv, q_pos0, d, d_v, k, causal
+
+
+@pytest.mark.parametrize("i", range(32))
+def test_random_shape_backward(lib, i):
+    """The backward (straight-through rule) on 32 seeded random shapes, with test_gpu_bwd's componentwise
+    and normwise bounds (reading A24) and its bitwise determinism check."""
+    from test_gpu_bwd import check, run_bwd
+    B, H, H_kv, n, n_kv, q_pos0, d, d_v, k, causal = draw_bwd(i)
+    gpu, ref = run_bwd(lib, 900 + i, B, H, H_kv, n, d, d_v, k, causal=causal, q_pos0=q_pos0, n_kv=n_kv)
+    check(gpu, ref)
